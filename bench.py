@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark of the Oregonator forward-Euler hot path (BASELINE.json metric:
+"Gcell-updates/s and % of B200 HBM roofline at 1/2/4/8 GPUs").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One bench "step" = rd_step(T) with T = --timesteps (default 1000) time steps of
+the whole hot path (a1-a8: due stimuli, K-step blocked stencil launches, the
+non-finite health check, probe latches) over the workload:
+  N = 1: configs[3] "c4_roofline" 16384 x 16384 fp32, noise + 64 half-discs;
+         K = 10 x 1000 = the config's 10000 timed steps.
+  N > 1: configs[4] weak scaling: a 16384-row slab per GPU of a
+         (16384 N) x 16384 grid with 16 N obstacles, halo exchange over NCCL.
+Inputs (5 planes x 1 GiB per GPU) are far larger than L2 (126 MB), so no
+flush is needed between steps. Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gcell-updates/s and % of B200 HBM roofline at 1/2/4/8 GPUs"
+UNIT = "Gcell-updates/s"
+BYTES_PER_CELL = {np.dtype(np.float32): 20, np.dtype(np.float64): 40}  # read u,v,phi + write u,v
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import paper_1901_06535_b200 as rd
+    from paper_1901_06535_b200.dist import SlabSim
+    from rdinputs import config
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = np.dtype(np.float32)
+    T = args.timesteps
+    hbm, hbm_src = peaks()
+
+    if world == 1:
+        w = config(4)
+        H, W = w.H, w.W
+        u0, v0 = w.init_planes(0)
+        phi = w.phi_plane(0).astype(dtype)
+        sim = rd.Sim(phi, dtype=dtype, tb_depth=args.tb)
+        h = sim.h
+        sim.write(0, u0, v0)
+        for shape, val, at in w.events[0]:
+            sim.stimulate(shape, val, at)
+        stepper = sim.step
+        cells = H * W
+        workload = {"workload": "configs[3] c4_roofline: 16384x16384 fp32, phi=0.054, u,v~U[0,0.1) seed 1, "
+                                "64 half-discs r=8 seed 2, no-flux", "grid": [H, W]}
+    else:
+        w = config(5, H=16384 * world, W=16384, n_obstacles=16 * world)
+        H, W = w.H, w.W
+        slab = SlabSim(W, H, rank, world, lambda b, r0, n: w.phi_plane(0, r0, n), dtype=dtype,
+                       halo=max(args.tb, 4) if args.tb else 4)
+        h = slab.h
+        slab.write(0, lambda b, r0, n: w.init_planes(0, r0, n)[0], lambda b, r0, n: w.init_planes(0, r0, n)[1])
+        for shape, val, at in w.events[0]:
+            slab.stimulate(shape, val, at)
+        stepper = slab.step
+        cells = slab.rows * W
+        u0 = v0 = None
+        workload = {"workload": f"configs[4] weak scaling: ({H})x{W} fp32 row slabs, 16 obstacles/GPU phi=0.2, "
+                                "masked half-discs, NCCL halo exchange", "grid": [H, W]}
+    stream = torch.cuda.current_stream()
+    rd.rd_set_stream(h, stream.cuda_stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        stepper(T)
+    barrier()
+    rd.rd_reset_stats(h)
+    rd.rd_set_profiling(h, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            stepper(T)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    st = rd.rd_get_stats(h)
+    rd.rd_set_profiling(h, False)
+    ms_max = ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    total_updates = cells * world * T * args.steps
+    value = total_updates / (ms_max / 1e3) / 1e9
+
+    # dominant kernel: the temporally blocked stencil (tb_kernel)
+    kms = st["step_kernel_ms"]
+    k_launches = max(1, st["timed_launches"])
+    bpc = BYTES_PER_CELL[dtype]
+    achieved = bpc * st["cell_updates"] / (kms / 1e3) / 1e9 if kms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                "kernel": f"tb_kernel<float,K={st['tb_depth']}>", "peak_source": hbm_src,
+                "algorithmic_bytes_per_cell_update": bpc,
+                "cell_updates_per_launch": st["cell_updates"] / k_launches,
+                "avg_launch_ms": kms / k_launches, "kernel_share_of_step": kms / ms if ms else None,
+                "one_step_roofline_gcells": hbm / bpc}
+
+    # e2e through the public C ABI with pinned host buffers (1 GPU only)
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        pu = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+        pv = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+        pu[...] = u0
+        pv[...] = v0
+        ou = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+        ov = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            rd.rd_write_fields(h, 0, pu, pv)
+            rd.rd_step(h, T)
+            rd.rd_read_fields(h, 0, ou, ov)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(b)
+        e2e = {"value": cells * T * args.e2e_steps / (ems / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * cells * 4, "d2h_bytes_per_step": 2 * cells * 4,
+               "steps": args.e2e_steps, "api": "rd_write_fields(host pinned) + rd_step + rd_read_fields(host)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(u0, v0, phi, args.cpu_seconds)
+
+    launches = st["launches"]
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": dict(workload, time_steps_per_step=T, tb_depth=st["tb_depth"],
+                               l2="inputs larger than L2 (5 x 1 GiB planes per GPU); no flush needed",
+                               parallelism=f"row slabs x{world}" if world > 1 else "single GPU"),
+                "frac_of_one_step_hbm_roofline": value / world / (hbm / bpc),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(u0, v0, phi, seconds: float):
+    """The oracle, as it stands, on the host cores: a bounded sample of the same
+    workload (the full grid for a few time steps, fp32 mode)."""
+    import oracle
+    H, W = u0.shape
+    t = time.perf_counter()
+    oracle.run(u0, v0, phi, 1)
+    t1 = time.perf_counter() - t
+    n = int(max(1, min(20, seconds / max(t1, 1e-3))))
+    t = time.perf_counter()
+    oracle.run(u0, v0, phi, n)
+    el = time.perf_counter() - t
+    return {"value": H * W * n / el / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"full {H}x{W} grid, {n} time steps, fp32 mode (config-4 inputs, no stimuli)",
+            "seconds": el}
+
+
+# ------------------------------------------------------- reference arm
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) timed as it
+    stands on the host cores, on our arm's config/metric/unit. Each step is a
+    bounded sample: one time step of the full 16384^2 fp32 grid."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from rdinputs import config
+    w = config(4)
+    u, v = w.init_planes(0)
+    phi = w.phi_plane(0).astype(np.float32)
+    n = 1
+    for _ in range(args.warmup):
+        r = oracle.run(u, v, phi, n, events=w.events[0])
+    t = time.perf_counter()
+    cu, cv = u, v
+    for s in range(args.steps):
+        r = oracle.run(cu, cv, phi, n, events=w.events[0], step0=s)
+        cu, cv = r.u, r.v
+    el = time.perf_counter() - t
+    value = w.H * w.W * n * args.steps / el / 1e9
+    cfg = {"workload": "configs[3] c4_roofline: 16384x16384 fp32 (oracle fp32 mode)", "grid": [w.H, w.W],
+           "time_steps_per_step": n}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"{n} time step(s) of the full grid per bench step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--timesteps", type=int, default=1000, help="time steps per bench step")
+    ap.add_argument("--tb", type=int, default=0, help="temporal-blocking depth (0 = auto)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,237 @@
+/*
+ * rd.h — C ABI of the B200-native Oregonator reaction-diffusion engine.
+ *
+ * The hot path is explicit forward-Euler
+ * time stepping of the two-variable Oregonator model, §2 Eq. 1
+ * (PAPER.md:89-94):
+ *     du/dt = (1/eps) [u - u^2 - (f v + phi(x,y)) (u - q)/(u + q)] + Du Lap(u)
+ *     dv/dt = u - v
+ * integrated "using an explicit forward Euler integration, with timestep dt
+ * and five-node discrete Laplace operator with grid spacing dx"
+ * (PAPER.md:122-124), with "catalytic stimulation ... by setting the
+ * excitatory concentration (u) of stimulated pixels to 1.0".
+ * Default parameters: Table 1.
+ *
+ * All entry points are plain C: opaque handle, plain host/device pointers and
+ * sizes, int status codes (RD_OK = 0 or a negative RD_E* code). The handle
+ * owns all device memory it allocates. Handles are not thread-safe (one
+ * writer per handle). Work is issued on the handle's CUDA stream; every call
+ * that returns data to the host synchronises that stream. A failing call
+ * leaves a message for rd_last_error().
+ *
+ * Numerics: every binary floating-point operation is rounded
+ * separately in the handle's precision (no FMA contraction), in the order
+ *   L  = (((N + S) + (E + W)) - 4*C) * INV_DX2
+ *   r  = (C - Q) / (C + Q)                          (IEEE division)
+ *   R  = (C - C*C) - ((F*v + phi) * r)
+ *   u' = C + DT * ((R * INV_EPS) + (DU * L))        v' = v + DT * (C - v)
+ * with out-of-grid neighbours := the edge cell (no-flux), and every constant
+ * computed in fp64 from rd_params and rounded once to the precision.
+ * Results are bitwise independent of temporal-blocking depth, batching,
+ * rd_step splitting and slab decomposition.
+ */
+#ifndef RD_H
+#define RD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RD_ABI_VERSION 1
+
+typedef struct rd_sim rd_sim; /* opaque handle */
+
+/* ---- status codes ---- */
+enum {
+  RD_OK = 0,
+  RD_EINVAL = -1,      /* null pointer, dims < 3, batch < 1, bad kind/dtype, radius < 0 */
+  RD_EPARAM = -2,      /* parameter invariants violated: all > 0, q < 1, dt*Du/dx^2 < 0.25 */
+  RD_ERANGE = -3,      /* probe rect empty/outside the grid, at_step < current step, instance out of range */
+  RD_ENONFINITE = -4,  /* non-finite input, or produced during rd_step; see rd_last_error / rd_get_fault */
+  RD_ECUDA = -5,       /* CUDA runtime error (message has the CUDA error string) */
+  RD_ENOMEM = -7       /* device or host allocation failed */
+};
+
+/* ---- precisions ---- */
+enum { RD_F32 = 1, RD_F64 = 2 };
+
+/* ---- rd_grid.flags ---- */
+enum {
+  RD_REACTION_OFF = 1u,   /* integrate u' = u + dt*Du*L, v' = v (diffusion-only conservation pin) */
+  RD_NO_CHECKPOINT = 2u,  /* skip the per-rd_step checkpoint: faults are then reported at k-block
+                             granularity and the fields are left at the end of the failing block */
+  RD_NO_GRAPH = 4u        /* never replay rd_step segments through CUDA graphs */
+};
+
+/* ---- stimulus shape kinds ---- */
+enum { RD_DISC = 1, RD_RECT = 2, RD_HALF_DISC = 3 };
+enum { RD_SHAPE_MASK_PHI = 1u }; /* rd_shape.flags: write only cells whose phi == mask_phi */
+
+/* Model parameters of Eq. 1 and its discretisation; Table 1 defaults via
+ * rd_params_default. phi is per cell (the phi map). */
+typedef struct {
+  double eps, f, q, Du, dt, dx;
+} rd_params;
+
+/* Grid description. An instance is a height x width row-major grid; `batch`
+ * independent instances (e.g. the AND-gate truth-table rows, BASELINE.json
+ * configs[1]) are stepped together. tb_depth = time steps per HBM round trip
+ * (0 = automatic; results do not depend on it). pitch = elements between
+ * rows in device memory (0 = automatic, a multiple of 32). */
+typedef struct {
+  int64_t width, height;
+  int32_t batch;
+  int32_t dtype;    /* RD_F32 | RD_F64 */
+  int32_t tb_depth; /* 0 = auto, else 1..RD_MAX_TB */
+  uint32_t flags;   /* RD_REACTION_OFF | RD_NO_CHECKPOINT | RD_NO_GRAPH */
+  int64_t pitch;
+} rd_grid;
+
+#define RD_MAX_TB 8
+
+/* Stimulus shape, integer geometry (R-14). Cell (i, j) = (row, col).
+ *   RD_DISC       (2i - cy2)^2 + (2j - cx2)^2 <= 4 r^2   (centre in half cells)
+ *   RD_RECT       y0 <= i < y1 and x0 <= j < x1
+ *   RD_HALF_DISC  the disc and (2j-cx2)*dx + (2i-cy2)*dy >= 0,
+ *                 (dx,dy) = (1,0),(0,1),(-1,0),(0,-1) for dir 0..3
+ * Shapes are clipped to the grid. With RD_SHAPE_MASK_PHI only
+ * cells whose phi equals mask_phi (rounded to the precision) are written. */
+typedef struct {
+  int32_t kind;
+  int32_t dir;
+  int64_t cy2, cx2, r;
+  int64_t y0, x0, y1, x1;
+  uint32_t flags;
+  uint32_t reserved;
+  double mask_phi;
+} rd_shape;
+
+/* Axis-aligned probe rectangle [y0, y1) x [x0, x1). */
+typedef struct {
+  int64_t y0, x0, y1, x1;
+} rd_rect;
+
+/* First non-finite cell reported by rd_step (step after which it appeared). */
+typedef struct {
+  int64_t step;
+  int32_t b;
+  int32_t pad;
+  int64_t i, j;
+} rd_fault;
+
+/* Kernel-level statistics for the measurement harness (bench.py). */
+typedef struct {
+  int64_t launches;        /* kernels this library launched since creation / last reset */
+  int64_t step_launches;   /* of which stencil (time-step) kernels */
+  int64_t cell_updates;    /* cell-updates performed by the stencil kernels (owned cells x steps) */
+  double step_kernel_ms;   /* summed CUDA-event durations of stencil launches (profiling on) */
+  int64_t timed_launches;  /* stencil launches covered by step_kernel_ms */
+  int32_t tb_depth;        /* temporal-blocking depth in use */
+  int32_t pad;
+} rd_stats;
+
+/* ---- lifecycle ---- */
+
+/* Table 1 defaults: eps=0.0243, f=1.4, q=0.002, Du=0.45, dt=0.001, dx=0.25. */
+void rd_params_default(rd_params* p);
+
+/* Create a handle. phi_map: HOST buffer [batch][height][width] of the grid's
+ * dtype (copied; must be finite). u = v = 0 initially (R-10).
+ * Errors: RD_EINVAL, RD_EPARAM, RD_ENONFINITE (phi), RD_ENOMEM, RD_ECUDA. */
+int rd_create(const rd_grid* grid, const rd_params* params, const void* phi_map, struct rd_sim** out);
+
+/* Release all device memory and the stream (if owned). NULL is a no-op. */
+int rd_destroy(struct rd_sim* sim);
+
+/* Use an external CUDA stream (cudaStream_t, e.g. torch's current stream)
+ * for all subsequent work; NULL reverts to the handle's own stream. */
+int rd_set_stream(struct rd_sim* sim, void* cuda_stream);
+
+/* ---- state I/O (HOST buffers, [height][width] of dtype, row-major) ---- */
+
+/* Overwrite instance b's u and/or v (either may be NULL). Values must be finite. */
+int rd_write_fields(struct rd_sim* sim, int32_t b, const void* u, const void* v);
+
+/* Copy instance b's current u and/or v to host (either may be NULL). Syncs. */
+int rd_read_fields(struct rd_sim* sim, int32_t b, void* u_out, void* v_out);
+
+/* Same with DEVICE buffers (pitch = width, dtype elements); async on the stream. */
+int rd_read_fields_device(struct rd_sim* sim, int32_t b, void* u_out, void* v_out);
+int rd_write_fields_device(struct rd_sim* sim, int32_t b, const void* u, const void* v);
+
+/* ---- stimulation (a1) ---- */
+
+/* Schedule u := value on the shape's cells of instance b (-1 = all) before
+ * step at_step+1 is integrated, i.e. after at_step steps have completed
+ * (SPEC.md:438). Events at the same step apply in submission order.
+ * Errors: RD_EINVAL (shape), RD_ERANGE (at_step < current step, b out of range). */
+int rd_stimulate(struct rd_sim* sim, int32_t b, const rd_shape* shape, double value, int64_t at_step);
+
+/* ---- time stepping (a2-a8) ---- */
+
+/* Advance all instances by n >= 0 steps. Applies due
+ * stimuli, latches probes after every multiple of their stride, and checks
+ * for non-finite cells. Returns RD_ENONFINITE if any cell became non-finite:
+ * then (unless RD_NO_CHECKPOINT) the handle holds the state right after the
+ * first failing step, rd_get_step() is that step and rd_get_fault() names the
+ * first non-finite cell in (b, i, j) row-major order. rd_step(a); rd_step(b)
+ * is bitwise identical to rd_step(a+b). */
+int rd_step(struct rd_sim* sim, int64_t n);
+
+int64_t rd_get_step(const struct rd_sim* sim);
+int rd_get_fault(const struct rd_sim* sim, rd_fault* out);
+
+/* ---- probes (a6) ---- */
+
+/* Immediate probe: max of u over rect of instance b; fired = max >= threshold
+ * (SPEC.md:243-247). Syncs. */
+int rd_probe(struct rd_sim* sim, int32_t b, const rd_rect* rect, double threshold, int32_t* fired,
+             double* max_u);
+
+/* Latched probe: evaluated after every step that is a positive multiple of
+ * stride, remembers the first such step with
+ * max u >= threshold. Returns its id in *id. */
+int rd_probe_latch(struct rd_sim* sim, int32_t b, const rd_rect* rect, double threshold, int32_t stride,
+                   int32_t* id);
+
+/* First firing step of latched probe id, or -1 if it has not fired. Syncs. */
+int rd_probe_result(struct rd_sim* sim, int32_t id, int64_t* first_fire_step);
+
+/* ---- row slabs for multi-GPU domain decomposition ---- */
+
+/* Create a handle owning rows [row0, row0 + grid->height) of a grid with
+ * height_global rows, with `halo` ghost rows above and below (halo >= the
+ * temporal-blocking depth). phi_slab: HOST [batch][rows][width] for the rows
+ * [max(0,row0-halo), min(height_global, row0+height+halo)). Ghost rows at
+ * interior slab edges must be refreshed by the caller after every rd_step
+ * (n <= halo per call); global top/bottom edges use the no-flux clamp. */
+int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi_slab, int64_t row0,
+                   int64_t height_global, int32_t halo, struct rd_sim** out);
+
+/* Device pointer to local row `row` (-halo <= row < height + halo) of instance
+ * b's CURRENT u (plane 0) or v (plane 1), and the row pitch in bytes. The
+ * pointer is valid until the next rd_step (buffers ping-pong). */
+int rd_row_ptr(struct rd_sim* sim, int32_t b, int32_t plane, int64_t row, void** ptr, int64_t* pitch_bytes);
+
+/* ---- measurement ---- */
+
+/* Enable per-launch CUDA-event timing of stencil kernels (bench.py only). */
+int rd_set_profiling(struct rd_sim* sim, int32_t on);
+int rd_get_stats(struct rd_sim* sim, rd_stats* out);
+int rd_reset_stats(struct rd_sim* sim);
+
+/* Per-handle message of the last failing call ("" if none). */
+const char* rd_last_error(const struct rd_sim* sim);
+
+/* Message of the last failing rd_create* (no handle yet). */
+const char* rd_create_error(void);
+
+int32_t rd_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RD_H */

@@ -1,0 +1,255 @@
+"""B200-native Oregonator reaction-diffusion engine (RDCSim hot path, arXiv 1901.06535).
+
+Thin Python binding of the C ABI in include/rd.h. The module-level functions
+carry the C names (rd_create, rd_stimulate, rd_step, rd_read_fields, rd_probe,
+...) and only marshal arguments; ``Sim`` is a convenience wrapper over them.
+Every step of the hot path runs in librd.so's sm_100a kernels; if the
+extension is missing, calls raise (there is no CPU fallback).
+
+PyTorch is optional here and only used for streams (``Sim.set_stream``) and
+process groups (``paper_1901_06535_b200.dist``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_CHECKPOINT,  # noqa: F401
+                   RD_NO_GRAPH, RD_OK, RD_REACTION_OFF, RD_RECT, RD_SHAPE_MASK_PHI, load)
+
+__all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
+           "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
+           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_get_stats", "rd_set_profiling",
+           "rd_reset_stats", "rd_last_error", "load"]
+
+_KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
+_DT = {np.dtype(np.float32): RD_F32, np.dtype(np.float64): RD_F64}
+
+
+class RDError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_lib.ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _check(rc: int, handle=None, create: bool = False):
+    if rc != RD_OK:
+        L = load()
+        msg = (L.rd_create_error() if create else L.rd_last_error(handle)) or b""
+        raise RDError(rc, msg.decode(errors="replace"))
+
+
+def _ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags.c_contiguous
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _shape(s: dict) -> _lib.rd_shape:
+    out = _lib.rd_shape()
+    out.kind = _KIND[s["kind"]]
+    out.dir = int(s.get("dir", 0))
+    for k in ("cy2", "cx2", "r", "y0", "x0", "y1", "x1"):
+        setattr(out, k, int(s.get(k, 0)))
+    if s.get("mask_phi") is not None:
+        out.flags = RD_SHAPE_MASK_PHI
+        out.mask_phi = float(s["mask_phi"])
+    return out
+
+
+# ----------------------------------------------------------------- C names
+
+def rd_params_default() -> _lib.rd_params:
+    p = _lib.rd_params()
+    load().rd_params_default(C.byref(p))
+    return p
+
+
+def rd_create(width: int, height: int, phi_map: np.ndarray, *, batch: int = 1, dtype=np.float32,
+              tb_depth: int = 0, flags: int = 0, params: _lib.rd_params | None = None, pitch: int = 0):
+    """rd_create(grid, params, phi_map): phi_map is [batch][height][width] on the host."""
+    dt = np.dtype(dtype)
+    phi = np.ascontiguousarray(phi_map, dtype=dt)
+    assert phi.size == batch * height * width
+    g = _lib.rd_grid(width, height, batch, _DT[dt], tb_depth, flags, pitch)
+    p = params or rd_params_default()
+    h = C.c_void_p()
+    _check(load().rd_create(C.byref(g), C.byref(p), _ptr(phi), C.byref(h)), create=True)
+    return h
+
+
+def rd_create_slab(width: int, height: int, phi_slab: np.ndarray, row0: int, height_global: int, halo: int, *,
+                   batch: int = 1, dtype=np.float32, tb_depth: int = 0, flags: int = 0, params=None):
+    dt = np.dtype(dtype)
+    phi = np.ascontiguousarray(phi_slab, dtype=dt)
+    g = _lib.rd_grid(width, height, batch, _DT[dt], tb_depth, flags, 0)
+    p = params or rd_params_default()
+    h = C.c_void_p()
+    _check(load().rd_create_slab(C.byref(g), C.byref(p), _ptr(phi), row0, height_global, halo, C.byref(h)),
+           create=True)
+    return h
+
+
+def rd_destroy(h) -> None:
+    _check(load().rd_destroy(h), h)
+
+
+def rd_set_stream(h, stream_ptr: int | None) -> None:
+    _check(load().rd_set_stream(h, C.c_void_p(stream_ptr) if stream_ptr else None), h)
+
+
+def rd_stimulate(h, b: int, shape: dict, value: float = 1.0, at_step: int = 0) -> None:
+    s = _shape(shape)
+    _check(load().rd_stimulate(h, b, C.byref(s), float(value), int(at_step)), h)
+
+
+def rd_step(h, n: int) -> None:
+    _check(load().rd_step(h, int(n)), h)
+
+
+def rd_get_step(h) -> int:
+    return int(load().rd_get_step(h))
+
+
+def rd_get_fault(h) -> tuple:
+    f = _lib.rd_fault()
+    _check(load().rd_get_fault(h, C.byref(f)), h)
+    return (f.step, f.b, f.i, f.j)
+
+
+def rd_read_fields(h, b: int, u_out: np.ndarray | None, v_out: np.ndarray | None) -> None:
+    _check(load().rd_read_fields(h, b, _ptr(u_out), _ptr(v_out)), h)
+
+
+def rd_write_fields(h, b: int, u: np.ndarray | None, v: np.ndarray | None) -> None:
+    _check(load().rd_write_fields(h, b, _ptr(u), _ptr(v)), h)
+
+
+def rd_read_fields_device(h, b: int, u_ptr: int | None, v_ptr: int | None) -> None:
+    _check(load().rd_read_fields_device(h, b, C.c_void_p(u_ptr) if u_ptr else None,
+                                        C.c_void_p(v_ptr) if v_ptr else None), h)
+
+
+def rd_write_fields_device(h, b: int, u_ptr: int | None, v_ptr: int | None) -> None:
+    _check(load().rd_write_fields_device(h, b, C.c_void_p(u_ptr) if u_ptr else None,
+                                         C.c_void_p(v_ptr) if v_ptr else None), h)
+
+
+def rd_probe(h, b: int, rect, threshold: float = 0.1) -> tuple[bool, float]:
+    r = _lib.rd_rect(*rect)
+    fired, m = C.c_int32(), C.c_double()
+    _check(load().rd_probe(h, b, C.byref(r), float(threshold), C.byref(fired), C.byref(m)), h)
+    return bool(fired.value), m.value
+
+
+def rd_probe_latch(h, b: int, rect, threshold: float = 0.1, stride: int = 50) -> int:
+    r = _lib.rd_rect(*rect)
+    pid = C.c_int32()
+    _check(load().rd_probe_latch(h, b, C.byref(r), float(threshold), int(stride), C.byref(pid)), h)
+    return pid.value
+
+
+def rd_probe_result(h, pid: int) -> int:
+    out = C.c_int64()
+    _check(load().rd_probe_result(h, pid, C.byref(out)), h)
+    return out.value
+
+
+def rd_row_ptr(h, b: int, plane: int, row: int) -> tuple[int, int]:
+    p, pitch = C.c_void_p(), C.c_int64()
+    _check(load().rd_row_ptr(h, b, plane, row, C.byref(p), C.byref(pitch)), h)
+    return p.value, pitch.value
+
+
+def rd_set_profiling(h, on: bool) -> None:
+    _check(load().rd_set_profiling(h, 1 if on else 0), h)
+
+
+def rd_get_stats(h) -> dict:
+    s = _lib.rd_stats()
+    _check(load().rd_get_stats(h, C.byref(s)), h)
+    return {k: getattr(s, k) for k, _ in s._fields_ if k != "pad"}
+
+
+def rd_reset_stats(h) -> None:
+    _check(load().rd_reset_stats(h), h)
+
+
+def rd_last_error(h) -> str:
+    return (load().rd_last_error(h) or b"").decode(errors="replace")
+
+
+# ------------------------------------------------------------- convenience
+
+class Sim:
+    """Owning wrapper over an rd_sim handle (one instance batch on one GPU)."""
+
+    def __init__(self, phi: np.ndarray, *, dtype=np.float32, tb_depth: int = 0, flags: int = 0,
+                 params=None, pitch: int = 0):
+        phi = np.asarray(phi)
+        if phi.ndim == 2:
+            phi = phi[None]
+        self.B, self.H, self.W = phi.shape
+        self.dtype = np.dtype(dtype)
+        self.h = rd_create(self.W, self.H, phi, batch=self.B, dtype=dtype, tb_depth=tb_depth, flags=flags,
+                           params=params, pitch=pitch)
+
+    def close(self):
+        if getattr(self, "h", None):
+            rd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def stimulate(self, shape: dict, value: float = 1.0, at_step: int = 0, b: int = -1):
+        rd_stimulate(self.h, b, shape, value, at_step)
+
+    def step(self, n: int):
+        rd_step(self.h, n)
+
+    @property
+    def step_count(self) -> int:
+        return rd_get_step(self.h)
+
+    def read(self, b: int = 0):
+        u = np.empty((self.H, self.W), dtype=self.dtype)
+        v = np.empty((self.H, self.W), dtype=self.dtype)
+        rd_read_fields(self.h, b, u, v)
+        return u, v
+
+    def write(self, b: int, u: np.ndarray | None, v: np.ndarray | None):
+        rd_write_fields(self.h, b, None if u is None else np.ascontiguousarray(u, dtype=self.dtype),
+                        None if v is None else np.ascontiguousarray(v, dtype=self.dtype))
+
+    def probe(self, b: int, rect, threshold: float = 0.1):
+        return rd_probe(self.h, b, rect, threshold)
+
+    def probe_latch(self, b: int, rect, threshold: float = 0.1, stride: int = 50) -> int:
+        return rd_probe_latch(self.h, b, rect, threshold, stride)
+
+    def probe_result(self, pid: int) -> int:
+        return rd_probe_result(self.h, pid)
+
+    def fault(self):
+        return rd_get_fault(self.h)
+
+    def set_stream(self, stream) -> None:
+        """Issue work on a torch.cuda.Stream (or raw cudaStream_t int)."""
+        ptr = getattr(stream, "cuda_stream", stream)
+        rd_set_stream(self.h, ptr)
+
+    def stats(self) -> dict:
+        return rd_get_stats(self.h)

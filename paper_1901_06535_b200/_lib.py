@@ -1,0 +1,101 @@
+"""ctypes declarations of include/rd.h (argument marshalling only).
+
+Every compute step runs in librd.so's CUDA kernels. There is no CPU fallback:
+if the extension is missing this module raises on first use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librd.so")
+
+RD_OK, RD_EINVAL, RD_EPARAM, RD_ERANGE, RD_ENONFINITE, RD_ECUDA, RD_ENOMEM = 0, -1, -2, -3, -4, -5, -7
+RD_F32, RD_F64 = 1, 2
+RD_REACTION_OFF, RD_NO_CHECKPOINT, RD_NO_GRAPH = 1, 2, 4
+RD_DISC, RD_RECT, RD_HALF_DISC = 1, 2, 3
+RD_SHAPE_MASK_PHI = 1
+RD_MAX_TB = 8
+
+ERRNAMES = {0: "RD_OK", -1: "RD_EINVAL", -2: "RD_EPARAM", -3: "RD_ERANGE", -4: "RD_ENONFINITE",
+            -5: "RD_ECUDA", -7: "RD_ENOMEM"}
+
+
+class rd_params(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("eps", "f", "q", "Du", "dt", "dx")]
+
+
+class rd_grid(C.Structure):
+    _fields_ = [("width", C.c_int64), ("height", C.c_int64), ("batch", C.c_int32), ("dtype", C.c_int32),
+                ("tb_depth", C.c_int32), ("flags", C.c_uint32), ("pitch", C.c_int64)]
+
+
+class rd_shape(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("dir", C.c_int32), ("cy2", C.c_int64), ("cx2", C.c_int64),
+                ("r", C.c_int64), ("y0", C.c_int64), ("x0", C.c_int64), ("y1", C.c_int64), ("x1", C.c_int64),
+                ("flags", C.c_uint32), ("reserved", C.c_uint32), ("mask_phi", C.c_double)]
+
+
+class rd_rect(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("y0", "x0", "y1", "x1")]
+
+
+class rd_fault(C.Structure):
+    _fields_ = [("step", C.c_int64), ("b", C.c_int32), ("pad", C.c_int32), ("i", C.c_int64), ("j", C.c_int64)]
+
+
+class rd_stats(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("step_launches", C.c_int64), ("cell_updates", C.c_int64),
+                ("step_kernel_ms", C.c_double), ("timed_launches", C.c_int64), ("tb_depth", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+# (name, restype, argtypes) of every symbol include/rd.h declares
+P, i32, i64, u32, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_double
+SYMBOLS = [
+    ("rd_abi_version", C.c_int32, []),
+    ("rd_params_default", None, [C.POINTER(rd_params)]),
+    ("rd_create", C.c_int, [C.POINTER(rd_grid), C.POINTER(rd_params), P, C.POINTER(P)]),
+    ("rd_create_slab", C.c_int, [C.POINTER(rd_grid), C.POINTER(rd_params), P, i64, i64, i32, C.POINTER(P)]),
+    ("rd_destroy", C.c_int, [P]),
+    ("rd_set_stream", C.c_int, [P, P]),
+    ("rd_write_fields", C.c_int, [P, i32, P, P]),
+    ("rd_read_fields", C.c_int, [P, i32, P, P]),
+    ("rd_read_fields_device", C.c_int, [P, i32, P, P]),
+    ("rd_write_fields_device", C.c_int, [P, i32, P, P]),
+    ("rd_stimulate", C.c_int, [P, i32, C.POINTER(rd_shape), dbl, i64]),
+    ("rd_step", C.c_int, [P, i64]),
+    ("rd_get_step", C.c_int64, [P]),
+    ("rd_get_fault", C.c_int, [P, C.POINTER(rd_fault)]),
+    ("rd_probe", C.c_int, [P, i32, C.POINTER(rd_rect), dbl, C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+    ("rd_probe_latch", C.c_int, [P, i32, C.POINTER(rd_rect), dbl, i32, C.POINTER(C.c_int32)]),
+    ("rd_probe_result", C.c_int, [P, i32, C.POINTER(C.c_int64)]),
+    ("rd_row_ptr", C.c_int, [P, i32, i32, i64, C.POINTER(P), C.POINTER(C.c_int64)]),
+    ("rd_set_profiling", C.c_int, [P, i32]),
+    ("rd_get_stats", C.c_int, [P, C.POINTER(rd_stats)]),
+    ("rd_reset_stats", C.c_int, [P]),
+    ("rd_last_error", C.c_char_p, [P]),
+    ("rd_create_error", C.c_char_p, []),
+]
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """dlopen librd.so and declare every rd.h symbol. Raises if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(f"CUDA extension {p} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                           " (there is no CPU fallback)")
+    lib = C.CDLL(p)
+    for name, res, args in SYMBOLS:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib

@@ -1,0 +1,816 @@
+// rd_runtime.cu — the C-ABI (include/rd.h) over the sm_100a kernels.
+//
+// PRODUCT CODE. The runtime owns device planes (u ping-pong, v ping-pong,
+// phi, checkpoint), the pending stimulus queue, latched probes and the fault
+// word, and cuts every rd_step(n) into temporally blocked launches at event
+// and probe steps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rd.h"
+#include "rd_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct PendingEvent {
+  int32_t b;  // -1 = all
+  rdk::ShapeDev shape;
+  double value;
+  double mask_phi;
+  int64_t at;
+};
+
+struct LatchedProbe {
+  int32_t b;
+  rd_rect rect;
+  double threshold;
+  int32_t stride;
+};
+
+}  // namespace
+
+struct rd_sim {
+  rd_grid g{};
+  rd_params p{};
+  size_t esz = 4;
+  int64_t H = 0, W = 0, B = 0, pitch = 0, halo = 0, rows_alloc = 0, plane_stride = 0;
+  int64_t grow0 = 0, Hg = 0;
+  bool slab = false;
+  int top_edge = 1, bot_edge = 1;
+  int32_t r_lo = 0, r_hi = 0;
+  void* u[2] = {nullptr, nullptr};
+  void* v[2] = {nullptr, nullptr};
+  void* phi = nullptr;
+  void* ck_u = nullptr;
+  void* ck_v = nullptr;
+  int cur = 0;
+  int64_t step = 0;
+  int K = 4;
+  std::vector<PendingEvent> events;
+  std::vector<LatchedProbe> probes;
+  rdk::ProbeDev* d_probes = nullptr;
+  long long* d_first = nullptr;
+  long long* d_first_ck = nullptr;
+  int probes_cap = 0;
+  bool probes_dirty = false;
+  unsigned long long* d_fault = nullptr;
+  int* d_flag = nullptr;
+  void* d_scratch = nullptr;  // probe max output
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  size_t ev_used = 0;
+  rd_stats st{};
+  double acc_ms = 0.0;
+  int64_t acc_timed = 0;
+  rd_fault fault{-1, -1, 0, -1, -1};
+  std::string err;
+};
+
+namespace {
+
+int set_err(rd_sim* s, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (s)
+    s->err = buf;
+  else
+    g_create_error = buf;
+  return code;
+}
+
+#define RD_CUDA(sim, call)                                                                        \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return set_err((sim), e_ == cudaErrorMemoryAllocation ? RD_ENOMEM : RD_ECUDA, "%s: %s (%s:%d)", \
+                     #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+  } while (0)
+
+int check_params(const rd_params* p, std::string* why) {
+  const double v[6] = {p->eps, p->f, p->q, p->Du, p->dt, p->dx};
+  for (double x : v)
+    if (!(x > 0.0) || !std::isfinite(x)) {
+      *why = "all parameters must be finite and > 0 (SPEC.md:28)";
+      return RD_EPARAM;
+    }
+  if (!(p->q < 1.0)) {
+    *why = "q must be < 1 (SPEC.md:28)";
+    return RD_EPARAM;
+  }
+  if (!(p->dt * p->Du / (p->dx * p->dx) < 0.25)) {
+    *why = "dt*Du/dx^2 must be < 0.25 (explicit-scheme guard, SPEC.md:28)";
+    return RD_EPARAM;
+  }
+  return RD_OK;
+}
+
+template <typename T>
+rdk::Consts<T> make_consts(const rd_params& p) {
+  rdk::Consts<T> k;
+  k.inv_eps = (T)(1.0 / p.eps);
+  k.f = (T)p.f;
+  k.q = (T)p.q;
+  k.du = (T)p.Du;
+  k.dt = (T)p.dt;
+  k.inv_dx2 = (T)(1.0 / (p.dx * p.dx));
+  return k;
+}
+
+int auto_tb(const rd_sim* s) {
+  if (const char* e = getenv("RD_TB_DEPTH")) {
+    int k = atoi(e);
+    if (k >= 1 && k <= RD_MAX_TB) return k;
+  }
+  return s->esz == 4 ? 4 : 2;
+}
+
+template <typename T>
+constexpr int vec_of() {
+  return 16 / (int)sizeof(T);
+}
+
+int pick_hb(const rd_sim* s, int n_strips) {
+  if (const char* e = getenv("RD_HB")) {
+    int hb = atoi(e);
+    if (hb >= 1) return hb;
+  }
+  const int64_t target_tasks = 148 * 24;
+  int64_t hb = (s->H * (int64_t)n_strips * s->B + target_tasks - 1) / target_tasks;
+  hb = std::max<int64_t>(hb, 16);
+  hb = std::min<int64_t>(hb, 512);
+  hb = (hb + 7) / 8 * 8;
+  return (int)hb;
+}
+
+template <typename T, int K, bool REACT>
+cudaError_t launch_tb_t(rd_sim* s, int in, int out) {
+  constexpr int V = vec_of<T>();
+  using G = rdk::StripGeom<K, V>;
+  rdk::TBArgs<T> a;
+  a.u_in = (const T*)s->u[in];
+  a.v_in = (const T*)s->v[in];
+  a.phi = (const T*)s->phi;
+  a.u_out = (T*)s->u[out];
+  a.v_out = (T*)s->v[out];
+  a.plane_stride = s->plane_stride;
+  a.pitch = s->pitch;
+  a.H = (int32_t)s->H;
+  a.W = (int32_t)s->W;
+  a.halo = (int32_t)s->halo;
+  a.r_lo = s->r_lo;
+  a.r_hi = s->r_hi;
+  a.top_edge = s->top_edge;
+  a.bot_edge = s->bot_edge;
+  a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
+  a.hb = pick_hb(s, a.n_strips);
+  a.grow0 = s->grow0;
+  a.H_global = s->Hg;
+  a.k = make_consts<T>(s->p);
+  a.fault_key = s->d_fault;
+  const int warps = 4;
+  dim3 grid((a.n_strips + warps - 1) / warps, (unsigned)((s->H + a.hb - 1) / a.hb), (unsigned)s->B);
+  rdk::tb_kernel<T, K, V, REACT><<<grid, warps * 32, 0, s->stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, bool REACT>
+cudaError_t launch_tb_k(rd_sim* s, int k, int in, int out) {
+  switch (k) {
+    case 1: return launch_tb_t<T, 1, REACT>(s, in, out);
+    case 2: return launch_tb_t<T, 2, REACT>(s, in, out);
+    case 3: return launch_tb_t<T, 3, REACT>(s, in, out);
+    case 4: return launch_tb_t<T, 4, REACT>(s, in, out);
+    case 5: return launch_tb_t<T, 5, REACT>(s, in, out);
+    case 6: return launch_tb_t<T, 6, REACT>(s, in, out);
+    case 7: return launch_tb_t<T, 7, REACT>(s, in, out);
+    case 8: return launch_tb_t<T, 8, REACT>(s, in, out);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int launch_tb(rd_sim* s, int k) {
+  const int in = s->cur, out = s->cur ^ 1;
+  const bool react = !(s->g.flags & RD_REACTION_OFF);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (s->profiling) {
+    if (s->ev_used == s->ev_pool.size()) {
+      cudaEvent_t a, b;
+      RD_CUDA(s, cudaEventCreate(&a));
+      RD_CUDA(s, cudaEventCreate(&b));
+      s->ev_pool.push_back({a, b});
+    }
+    e0 = s->ev_pool[s->ev_used].first;
+    e1 = s->ev_pool[s->ev_used].second;
+    ++s->ev_used;
+    RD_CUDA(s, cudaEventRecord(e0, s->stream));
+  }
+  cudaError_t e;
+  if (s->esz == 4)
+    e = react ? launch_tb_k<float, true>(s, k, in, out) : launch_tb_k<float, false>(s, k, in, out);
+  else
+    e = react ? launch_tb_k<double, true>(s, k, in, out) : launch_tb_k<double, false>(s, k, in, out);
+  if (e != cudaSuccess) return set_err(s, RD_ECUDA, "tb_kernel<k=%d> launch: %s", k, cudaGetErrorString(e));
+  if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
+  s->cur = out;
+  s->st.launches++;
+  s->st.step_launches++;
+  s->st.cell_updates += s->B * s->H * s->W * (int64_t)k;
+  return RD_OK;
+}
+
+// Bounding box of a shape in global rows / columns, clipped to the grid.
+void shape_bbox(const rdk::ShapeDev& sh, int64_t Hg, int64_t W, int64_t* i0, int64_t* i1, int64_t* j0,
+                int64_t* j1) {
+  if (sh.kind == RD_RECT) {
+    *i0 = sh.y0, *i1 = sh.y1, *j0 = sh.x0, *j1 = sh.x1;
+  } else {
+    // (2i - cy2)^2 <= 4r^2  <=>  cy2 - 2r <= 2i <= cy2 + 2r
+    auto cdiv2 = [](int64_t a) { return a >= 0 ? (a + 1) / 2 : -((-a) / 2); };  // ceil(a/2)
+    auto fdiv2 = [](int64_t a) { return a >= 0 ? a / 2 : -((-a + 1) / 2); };   // floor(a/2)
+    *i0 = cdiv2(sh.cy2 - 2 * sh.r);
+    *i1 = fdiv2(sh.cy2 + 2 * sh.r) + 1;
+    *j0 = cdiv2(sh.cx2 - 2 * sh.r);
+    *j1 = fdiv2(sh.cx2 + 2 * sh.r) + 1;
+  }
+  *i0 = std::max<int64_t>(*i0, 0);
+  *j0 = std::max<int64_t>(*j0, 0);
+  *i1 = std::min<int64_t>(*i1, Hg);
+  *j1 = std::min<int64_t>(*j1, W);
+}
+
+int apply_event(rd_sim* s, const PendingEvent& ev) {
+  int64_t i0, i1, j0, j1;
+  shape_bbox(ev.shape, s->Hg, s->W, &i0, &i1, &j0, &j1);
+  // local rows that exist in this handle (owned + readable ghosts)
+  int64_t x0 = std::max<int64_t>(i0 - s->grow0, s->r_lo);
+  int64_t x1 = std::min<int64_t>(i1 - s->grow0, s->r_hi);
+  if (x0 >= x1 || j0 >= j1) return RD_OK;
+  const int32_t b0 = ev.b < 0 ? 0 : ev.b;
+  const int32_t nb = ev.b < 0 ? (int32_t)s->B : 1;
+  dim3 block(128);
+  dim3 grid((unsigned)((j1 - j0 + 127) / 128), (unsigned)(x1 - x0), (unsigned)nb);
+  if (s->esz == 4)
+    rdk::stamp_kernel<float><<<grid, block, 0, s->stream>>>(
+        (float*)s->u[s->cur], (const float*)s->phi, s->plane_stride, s->pitch, (int32_t)s->halo, s->grow0,
+        ev.shape, (float)ev.value, (float)ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
+  else
+    rdk::stamp_kernel<double><<<grid, block, 0, s->stream>>>(
+        (double*)s->u[s->cur], (const double*)s->phi, s->plane_stride, s->pitch, (int32_t)s->halo, s->grow0,
+        ev.shape, ev.value, ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
+  RD_CUDA(s, cudaGetLastError());
+  s->st.launches++;
+  return RD_OK;
+}
+
+int sync_probes(rd_sim* s) {
+  if (!s->probes_dirty) return RD_OK;
+  const int n = (int)s->probes.size();
+  if (n > s->probes_cap) {
+    int cap = std::max(8, 2 * n);
+    rdk::ProbeDev* dp = nullptr;
+    long long *df = nullptr, *dfc = nullptr;
+    RD_CUDA(s, cudaMalloc(&dp, sizeof(rdk::ProbeDev) * cap));
+    RD_CUDA(s, cudaMalloc(&df, sizeof(long long) * cap));
+    RD_CUDA(s, cudaMalloc(&dfc, sizeof(long long) * cap));
+    std::vector<long long> init(cap, -1);
+    RD_CUDA(s, cudaMemcpyAsync(df, init.data(), sizeof(long long) * cap, cudaMemcpyHostToDevice, s->stream));
+    if (s->d_first && s->probes_cap)
+      RD_CUDA(s, cudaMemcpyAsync(df, s->d_first, sizeof(long long) * s->probes_cap, cudaMemcpyDeviceToDevice,
+                                 s->stream));
+    RD_CUDA(s, cudaStreamSynchronize(s->stream));
+    cudaFree(s->d_probes);
+    cudaFree(s->d_first);
+    cudaFree(s->d_first_ck);
+    s->d_probes = dp;
+    s->d_first = df;
+    s->d_first_ck = dfc;
+    s->probes_cap = cap;
+  }
+  std::vector<rdk::ProbeDev> hp(n);
+  for (int i = 0; i < n; ++i) {
+    const LatchedProbe& q = s->probes[i];
+    // local owned rows only (slabs: each rank probes its own rows)
+    hp[i].y0 = std::max<int64_t>(q.rect.y0 - s->grow0, 0);
+    hp[i].y1 = std::min<int64_t>(q.rect.y1 - s->grow0, s->H);
+    if (hp[i].y1 < hp[i].y0) hp[i].y1 = hp[i].y0;
+    hp[i].x0 = q.rect.x0;
+    hp[i].x1 = q.rect.x1;
+    hp[i].b = q.b;
+    hp[i].stride = q.stride;
+    hp[i].threshold = q.threshold;
+  }
+  RD_CUDA(s, cudaMemcpyAsync(s->d_probes, hp.data(), sizeof(rdk::ProbeDev) * n, cudaMemcpyHostToDevice, s->stream));
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  s->probes_dirty = false;
+  return RD_OK;
+}
+
+int launch_probes(rd_sim* s, int64_t step) {
+  const int n = (int)s->probes.size();
+  if (!n) return RD_OK;
+  if (s->esz == 4)
+    rdk::probe_kernel<float><<<n, 256, 0, s->stream>>>((const float*)s->u[s->cur], s->plane_stride, s->pitch,
+                                                        (int32_t)s->halo, s->d_probes, n, step, s->d_first,
+                                                        nullptr);
+  else
+    rdk::probe_kernel<double><<<n, 256, 0, s->stream>>>((const double*)s->u[s->cur], s->plane_stride, s->pitch,
+                                                         (int32_t)s->halo, s->d_probes, n, step, s->d_first,
+                                                         nullptr);
+  RD_CUDA(s, cudaGetLastError());
+  s->st.launches++;
+  return RD_OK;
+}
+
+bool probe_due(const rd_sim* s, int64_t step) {
+  for (const auto& q : s->probes)
+    if (q.stride > 0 && step > 0 && step % q.stride == 0) return true;
+  return false;
+}
+
+// Advance from s->step to end with blocks of at most kmax steps.
+int run_range(rd_sim* s, int64_t end, int kmax) {
+  int rc = sync_probes(s);
+  if (rc) return rc;
+  while (s->step < end) {
+    // a1: stimuli due now, in submission order
+    for (size_t i = 0; i < s->events.size();) {
+      if (s->events[i].at == s->step) {
+        if ((rc = apply_event(s, s->events[i]))) return rc;
+        s->events.erase(s->events.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+    int64_t next = end;
+    for (const auto& ev : s->events)
+      if (ev.at > s->step) next = std::min(next, ev.at);
+    for (const auto& q : s->probes)
+      if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
+    while (s->step < next) {
+      const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      if ((rc = launch_tb(s, k))) return rc;
+      s->step += k;
+    }
+    if (probe_due(s, s->step))
+      if ((rc = launch_probes(s, s->step))) return rc;
+  }
+  return RD_OK;
+}
+
+int read_fault(rd_sim* s, unsigned long long* key) {
+  RD_CUDA(s, cudaMemcpyAsync(key, s->d_fault, sizeof(*key), cudaMemcpyDeviceToHost, s->stream));
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  return RD_OK;
+}
+
+int reset_fault(rd_sim* s) {
+  RD_CUDA(s, cudaMemsetAsync(s->d_fault, 0xff, sizeof(unsigned long long), s->stream));
+  return RD_OK;
+}
+
+int alloc_planes(rd_sim* s) {
+  const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
+  void** ps[5] = {&s->u[0], &s->u[1], &s->v[0], &s->v[1], &s->phi};
+  for (void** p : ps) {
+    RD_CUDA(s, cudaMalloc(p, bytes));
+    RD_CUDA(s, cudaMemsetAsync(*p, 0, bytes, s->stream));
+  }
+  if (!(s->g.flags & RD_NO_CHECKPOINT)) {
+    RD_CUDA(s, cudaMalloc(&s->ck_u, bytes));
+    RD_CUDA(s, cudaMalloc(&s->ck_v, bytes));
+  }
+  RD_CUDA(s, cudaMalloc(&s->d_fault, sizeof(unsigned long long)));
+  RD_CUDA(s, cudaMalloc(&s->d_flag, sizeof(int)));
+  RD_CUDA(s, cudaMalloc(&s->d_scratch, 64));
+  return reset_fault(s);
+}
+
+int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
+  RD_CUDA(s, cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream));
+  if (rows > 0) {
+    const int blocks = 148 * 8;
+    if (s->esz == 4)
+      rdk::finite_kernel<float><<<blocks, 256, 0, s->stream>>>((const float*)base, rows, s->W, s->pitch, s->d_flag);
+    else
+      rdk::finite_kernel<double><<<blocks, 256, 0, s->stream>>>((const double*)base, rows, s->W, s->pitch,
+                                                                 s->d_flag);
+    RD_CUDA(s, cudaGetLastError());
+    s->st.launches++;
+  }
+  RD_CUDA(s, cudaMemcpyAsync(bad, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  return RD_OK;
+}
+
+char* plane_ptr(rd_sim* s, void* plane, int64_t b, int64_t local_row) {
+  return (char*)plane + ((size_t)b * s->plane_stride + (size_t)(local_row + s->halo) * s->pitch) * s->esz;
+}
+
+int create_common(const rd_grid* grid, const rd_params* params, const void* phi_host, int64_t row0,
+                  int64_t Hg, int32_t halo, bool slab, rd_sim** out) {
+  if (!out) return set_err(nullptr, RD_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!grid || !params || !phi_host) return set_err(nullptr, RD_EINVAL, "grid, params and phi_map are required");
+  if (grid->width < 3 || grid->height < (slab ? 1 : 3))
+    return set_err(nullptr, RD_EINVAL, "width and height must be >= 3 (SPEC.md:32)");
+  if (grid->batch < 1) return set_err(nullptr, RD_EINVAL, "batch must be >= 1");
+  if (grid->dtype != RD_F32 && grid->dtype != RD_F64) return set_err(nullptr, RD_EINVAL, "dtype must be RD_F32 or RD_F64");
+  if (grid->tb_depth < 0 || grid->tb_depth > RD_MAX_TB) return set_err(nullptr, RD_EINVAL, "tb_depth must be 0..%d", RD_MAX_TB);
+  if (grid->width > (1ll << 31) - 1024 || grid->height > (1ll << 31) - 1024)
+    return set_err(nullptr, RD_EINVAL, "width/height must be < 2^31");
+  std::string why;
+  if (int rc = check_params(params, &why)) return set_err(nullptr, rc, "%s", why.c_str());
+  if (slab && (halo < 1 || halo > 64 || row0 < 0 || row0 + grid->height > Hg || Hg < 3))
+    return set_err(nullptr, RD_EINVAL, "bad slab geometry (row0, height_global, halo)");
+
+  rd_sim* s = new (std::nothrow) rd_sim();
+  if (!s) return set_err(nullptr, RD_ENOMEM, "host allocation failed");
+  s->g = *grid;
+  s->p = *params;
+  s->esz = grid->dtype == RD_F32 ? 4 : 8;
+  s->H = grid->height;
+  s->W = grid->width;
+  s->B = grid->batch;
+  s->pitch = grid->pitch > 0 ? grid->pitch : (grid->width + 31) / 32 * 32;
+  if (s->pitch < s->W || s->pitch % 32) {
+    delete s;
+    return set_err(nullptr, RD_EINVAL, "pitch must be >= width and a multiple of 32");
+  }
+  s->slab = slab;
+  s->halo = slab ? halo : 0;
+  s->grow0 = slab ? row0 : 0;
+  s->Hg = slab ? Hg : s->H;
+  s->top_edge = s->grow0 == 0;
+  s->bot_edge = s->grow0 + s->H == s->Hg;
+  s->r_lo = s->top_edge ? 0 : -(int32_t)s->halo;
+  s->r_hi = s->bot_edge ? (int32_t)s->H : (int32_t)(s->H + s->halo);
+  s->rows_alloc = s->H + 2 * s->halo;
+  s->plane_stride = s->rows_alloc * s->pitch;
+  s->K = grid->tb_depth > 0 ? grid->tb_depth : auto_tb(s);
+  if (slab && s->K > s->halo) s->K = (int)s->halo;
+  s->st.tb_depth = s->K;
+
+  auto fail = [&](int rc) {
+    std::string m = s->err;
+    rd_destroy(s);
+    return set_err(nullptr, rc, "%s", m.c_str());
+  };
+  if (cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    s->err = "cudaStreamCreate failed (no CUDA device?)";
+    return fail(RD_ECUDA);
+  }
+  s->stream = s->own_stream;
+  if (int rc = alloc_planes(s)) return fail(rc);
+  // phi rows present in the host buffer: local [lo, hi)
+  const int64_t lo = slab ? std::max<int64_t>(0, row0 - halo) - row0 : 0;
+  const int64_t hi = slab ? std::min<int64_t>(Hg, row0 + s->H + halo) - row0 : s->H;
+  for (int64_t b = 0; b < s->B; ++b) {
+    const char* src = (const char*)phi_host + (size_t)b * (hi - lo) * s->W * s->esz;
+    cudaError_t e = cudaMemcpy2DAsync(plane_ptr(s, s->phi, b, lo), s->pitch * s->esz, src, s->W * s->esz,
+                                      s->W * s->esz, hi - lo, cudaMemcpyHostToDevice, s->stream);
+    if (e != cudaSuccess) {
+      s->err = std::string("phi upload: ") + cudaGetErrorString(e);
+      return fail(RD_ECUDA);
+    }
+    int bad = 0;
+    if (int rc = check_finite_dev(s, plane_ptr(s, s->phi, b, lo), hi - lo, &bad)) return fail(rc);
+    if (bad) {
+      s->err = "phi_map contains non-finite values";
+      return fail(RD_ENONFINITE);
+    }
+  }
+  if (cudaStreamSynchronize(s->stream) != cudaSuccess) {
+    s->err = "stream sync failed";
+    return fail(RD_ECUDA);
+  }
+  *out = s;
+  return RD_OK;
+}
+
+int check_b(rd_sim* s, int32_t b) {
+  if (b < 0 || b >= s->B) return set_err(s, RD_ERANGE, "instance %d out of range [0,%lld)", b, (long long)s->B);
+  return RD_OK;
+}
+
+int copy_fields(rd_sim* s, int32_t b, void* uo, void* vo, cudaMemcpyKind kind, bool to_dev) {
+  void* planes[2] = {s->u[s->cur], s->v[s->cur]};
+  void* bufs[2] = {uo, vo};
+  for (int k = 0; k < 2; ++k) {
+    if (!bufs[k]) continue;
+    char* dev = plane_ptr(s, planes[k], b, 0);
+    if (to_dev)
+      RD_CUDA(s, cudaMemcpy2DAsync(dev, s->pitch * s->esz, bufs[k], s->W * s->esz, s->W * s->esz, s->H, kind,
+                                   s->stream));
+    else
+      RD_CUDA(s, cudaMemcpy2DAsync(bufs[k], s->W * s->esz, dev, s->pitch * s->esz, s->W * s->esz, s->H, kind,
+                                   s->stream));
+  }
+  return RD_OK;
+}
+
+int write_fields(rd_sim* s, int32_t b, const void* u, const void* v, cudaMemcpyKind kind) {
+  if (int rc = check_b(s, b)) return rc;
+  if (int rc = copy_fields(s, b, const_cast<void*>(u), const_cast<void*>(v), kind, true)) return rc;
+  void* planes[2] = {s->u[s->cur], s->v[s->cur]};
+  const void* bufs[2] = {u, v};
+  for (int k = 0; k < 2; ++k) {
+    if (!bufs[k]) continue;
+    int bad = 0;
+    if (int rc = check_finite_dev(s, plane_ptr(s, planes[k], b, 0), s->H, &bad)) return rc;
+    if (bad) return set_err(s, RD_ENONFINITE, "rd_write_fields: %s contains non-finite values", k ? "v" : "u");
+  }
+  return RD_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int32_t rd_abi_version(void) { return RD_ABI_VERSION; }
+
+void rd_params_default(rd_params* p) {
+  if (!p) return;
+  p->eps = 0.0243;
+  p->f = 1.4;
+  p->q = 0.002;
+  p->Du = 0.45;
+  p->dt = 0.001;
+  p->dx = 0.25;
+}
+
+const char* rd_create_error(void) { return g_create_error.c_str(); }
+
+const char* rd_last_error(const rd_sim* s) { return s ? s->err.c_str() : g_create_error.c_str(); }
+
+int rd_create(const rd_grid* grid, const rd_params* params, const void* phi_map, rd_sim** out) {
+  return create_common(grid, params, phi_map, 0, grid ? grid->height : 0, 0, false, out);
+}
+
+int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi_slab, int64_t row0,
+                   int64_t height_global, int32_t halo, rd_sim** out) {
+  return create_common(grid, params, phi_slab, row0, height_global, halo, true, out);
+}
+
+int rd_destroy(rd_sim* s) {
+  if (!s) return RD_OK;
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  void* ps[] = {s->u[0], s->u[1], s->v[0], s->v[1], s->phi, s->ck_u, s->ck_v, s->d_probes, s->d_first, s->d_first_ck,
+                s->d_fault, s->d_flag, s->d_scratch};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  for (auto& e : s->ev_pool) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (s->own_stream) cudaStreamDestroy(s->own_stream);
+  delete s;
+  return RD_OK;
+}
+
+int rd_set_stream(rd_sim* s, void* stream) {
+  if (!s) return RD_EINVAL;
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  s->stream = stream ? (cudaStream_t)stream : s->own_stream;
+  return RD_OK;
+}
+
+int rd_write_fields(rd_sim* s, int32_t b, const void* u, const void* v) {
+  if (!s) return RD_EINVAL;
+  return write_fields(s, b, u, v, cudaMemcpyHostToDevice);
+}
+
+int rd_write_fields_device(rd_sim* s, int32_t b, const void* u, const void* v) {
+  if (!s) return RD_EINVAL;
+  return write_fields(s, b, u, v, cudaMemcpyDeviceToDevice);
+}
+
+int rd_read_fields(rd_sim* s, int32_t b, void* u_out, void* v_out) {
+  if (!s) return RD_EINVAL;
+  if (int rc = check_b(s, b)) return rc;
+  if (int rc = copy_fields(s, b, u_out, v_out, cudaMemcpyDeviceToHost, false)) return rc;
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  return RD_OK;
+}
+
+int rd_read_fields_device(rd_sim* s, int32_t b, void* u_out, void* v_out) {
+  if (!s) return RD_EINVAL;
+  if (int rc = check_b(s, b)) return rc;
+  return copy_fields(s, b, u_out, v_out, cudaMemcpyDeviceToDevice, false);
+}
+
+int rd_stimulate(rd_sim* s, int32_t b, const rd_shape* shape, double value, int64_t at_step) {
+  if (!s) return RD_EINVAL;
+  if (!shape) return set_err(s, RD_EINVAL, "shape is NULL");
+  if (b < -1 || b >= s->B) return set_err(s, RD_ERANGE, "instance %d out of range", b);
+  if (at_step < s->step)
+    return set_err(s, RD_ERANGE, "at_step %lld is before the current step %lld", (long long)at_step, (long long)s->step);
+  if (shape->kind != RD_DISC && shape->kind != RD_RECT && shape->kind != RD_HALF_DISC)
+    return set_err(s, RD_EINVAL, "unknown shape kind %d", shape->kind);
+  if (shape->kind != RD_RECT && shape->r < 0) return set_err(s, RD_EINVAL, "radius must be >= 0 (SPEC.md:78)");
+  if (!std::isfinite(value)) return set_err(s, RD_ENONFINITE, "stimulus value is not finite");
+  PendingEvent ev;
+  ev.b = b;
+  ev.shape.kind = shape->kind;
+  ev.shape.dir = shape->dir;
+  ev.shape.cy2 = shape->cy2;
+  ev.shape.cx2 = shape->cx2;
+  ev.shape.r = shape->r;
+  ev.shape.y0 = shape->y0;
+  ev.shape.x0 = shape->x0;
+  ev.shape.y1 = shape->y1;
+  ev.shape.x1 = shape->x1;
+  ev.shape.mask = (shape->flags & RD_SHAPE_MASK_PHI) ? 1 : 0;
+  ev.value = value;
+  ev.mask_phi = shape->mask_phi;
+  ev.at = at_step;
+  s->events.push_back(ev);
+  return RD_OK;
+}
+
+int rd_step(rd_sim* s, int64_t n) {
+  if (!s) return RD_EINVAL;
+  if (n < 0) return set_err(s, RD_EINVAL, "n must be >= 0");
+  if (s->slab && n > s->halo) return set_err(s, RD_ERANGE, "slab handles step at most halo=%lld steps per call", (long long)s->halo);
+  if (n == 0) return RD_OK;
+  const bool ckpt = !(s->g.flags & RD_NO_CHECKPOINT);
+  const int64_t step0 = s->step;
+  const int cur0 = s->cur;
+  std::vector<PendingEvent> events0;
+  int rc = sync_probes(s);
+  if (rc) return rc;
+  if (ckpt) {
+    const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
+    RD_CUDA(s, cudaMemcpyAsync(s->ck_u, s->u[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
+    RD_CUDA(s, cudaMemcpyAsync(s->ck_v, s->v[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
+    if (!s->probes.empty())
+      RD_CUDA(s, cudaMemcpyAsync(s->d_first_ck, s->d_first, sizeof(long long) * s->probes.size(),
+                                 cudaMemcpyDeviceToDevice, s->stream));
+    events0 = s->events;
+  }
+  if ((rc = run_range(s, step0 + n, s->K))) return rc;
+  unsigned long long key = ~0ull;
+  if ((rc = read_fault(s, &key))) return rc;
+  if (key == ~0ull) return RD_OK;
+
+  if (ckpt) {
+    // Replay from the checkpoint one step per launch to find the first failing
+    // step exactly; the handle is left at that step (results are bitwise
+    // independent of the blocking depth, so the replay reproduces the run).
+    const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
+    s->cur = cur0;
+    RD_CUDA(s, cudaMemcpyAsync(s->u[s->cur], s->ck_u, bytes, cudaMemcpyDeviceToDevice, s->stream));
+    RD_CUDA(s, cudaMemcpyAsync(s->v[s->cur], s->ck_v, bytes, cudaMemcpyDeviceToDevice, s->stream));
+    if (!s->probes.empty())
+      RD_CUDA(s, cudaMemcpyAsync(s->d_first, s->d_first_ck, sizeof(long long) * s->probes.size(),
+                                 cudaMemcpyDeviceToDevice, s->stream));
+    s->events = events0;
+    s->step = step0;
+    if ((rc = reset_fault(s))) return rc;
+    key = ~0ull;
+    while (s->step < step0 + n) {
+      if ((rc = run_range(s, s->step + 1, 1))) return rc;
+      if ((rc = read_fault(s, &key))) return rc;
+      if (key != ~0ull) break;
+    }
+  }
+  const unsigned long long W = (unsigned long long)s->W, Hg = (unsigned long long)s->Hg;
+  s->fault.step = s->step;
+  s->fault.b = (int32_t)(key / (W * Hg));
+  s->fault.i = (int64_t)((key / W) % Hg);
+  s->fault.j = (int64_t)(key % W);
+  reset_fault(s);
+  return set_err(s, RD_ENONFINITE, "non-finite value at instance %d, cell (%lld, %lld) after step %lld%s", s->fault.b,
+                 (long long)s->fault.i, (long long)s->fault.j, (long long)s->fault.step,
+                 ckpt ? "" : " (k-block granularity: RD_NO_CHECKPOINT)");
+}
+
+int64_t rd_get_step(const rd_sim* s) { return s ? s->step : -1; }
+
+int rd_get_fault(const rd_sim* s, rd_fault* out) {
+  if (!s || !out) return RD_EINVAL;
+  *out = s->fault;
+  return RD_OK;
+}
+
+int rd_probe(rd_sim* s, int32_t b, const rd_rect* r, double threshold, int32_t* fired, double* max_u) {
+  if (!s || !r) return RD_EINVAL;
+  if (int rc = check_b(s, b)) return rc;
+  const int64_t y0 = r->y0 - s->grow0, y1 = r->y1 - s->grow0;
+  if (r->y0 >= r->y1 || r->x0 >= r->x1 || r->x0 < 0 || r->x1 > s->W || y0 < 0 || y1 > s->H)
+    return set_err(s, RD_ERANGE, "probe rect empty or outside the grid (SPEC.md:245-247)");
+  rdk::ProbeDev pd{y0, r->x0, y1, r->x1, b, 0, threshold};
+  rdk::ProbeDev* dp = (rdk::ProbeDev*)((char*)s->d_scratch);
+  static_assert(sizeof(rdk::ProbeDev) <= 48, "scratch");
+  RD_CUDA(s, cudaMemcpyAsync(dp, &pd, sizeof pd, cudaMemcpyHostToDevice, s->stream));
+  double m = 0;
+  if (s->esz == 4) {
+    float* mo = (float*)((char*)s->d_scratch + 48);
+    rdk::probe_kernel<float><<<1, 256, 0, s->stream>>>((const float*)s->u[s->cur], s->plane_stride, s->pitch,
+                                                        (int32_t)s->halo, dp, 1, s->step, nullptr, mo);
+    RD_CUDA(s, cudaGetLastError());
+    float h;
+    RD_CUDA(s, cudaMemcpyAsync(&h, mo, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+    RD_CUDA(s, cudaStreamSynchronize(s->stream));
+    m = h;
+    if (fired) *fired = h >= (float)threshold;
+  } else {
+    double* mo = (double*)((char*)s->d_scratch + 48);
+    rdk::probe_kernel<double><<<1, 256, 0, s->stream>>>((const double*)s->u[s->cur], s->plane_stride, s->pitch,
+                                                         (int32_t)s->halo, dp, 1, s->step, nullptr, mo);
+    RD_CUDA(s, cudaGetLastError());
+    RD_CUDA(s, cudaMemcpyAsync(&m, mo, sizeof m, cudaMemcpyDeviceToHost, s->stream));
+    RD_CUDA(s, cudaStreamSynchronize(s->stream));
+    if (fired) *fired = m >= threshold;
+  }
+  s->st.launches++;
+  if (max_u) *max_u = m;
+  return RD_OK;
+}
+
+int rd_probe_latch(rd_sim* s, int32_t b, const rd_rect* r, double threshold, int32_t stride, int32_t* id) {
+  if (!s || !r || !id) return RD_EINVAL;
+  if (int rc = check_b(s, b)) return rc;
+  if (stride < 1) return set_err(s, RD_EINVAL, "stride must be >= 1");
+  if (r->y0 >= r->y1 || r->x0 >= r->x1 || r->x0 < 0 || r->x1 > s->W || r->y0 < 0 || r->y1 > s->Hg)
+    return set_err(s, RD_ERANGE, "probe rect empty or outside the grid (SPEC.md:245-247)");
+  s->probes.push_back({b, *r, threshold, stride});
+  s->probes_dirty = true;
+  *id = (int32_t)s->probes.size() - 1;
+  return sync_probes(s);
+}
+
+int rd_probe_result(rd_sim* s, int32_t id, int64_t* first) {
+  if (!s || !first) return RD_EINVAL;
+  if (id < 0 || id >= (int32_t)s->probes.size()) return set_err(s, RD_ERANGE, "unknown probe id %d", id);
+  long long h = -1;
+  RD_CUDA(s, cudaMemcpyAsync(&h, s->d_first + id, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  *first = h;
+  return RD_OK;
+}
+
+int rd_row_ptr(rd_sim* s, int32_t b, int32_t plane, int64_t row, void** ptr, int64_t* pitch_bytes) {
+  if (!s || !ptr) return RD_EINVAL;
+  if (int rc = check_b(s, b)) return rc;
+  if (plane != 0 && plane != 1) return set_err(s, RD_EINVAL, "plane must be 0 (u) or 1 (v)");
+  if (row < -s->halo || row >= s->H + s->halo) return set_err(s, RD_ERANGE, "row %lld outside the slab", (long long)row);
+  *ptr = plane_ptr(s, plane == 0 ? s->u[s->cur] : s->v[s->cur], b, row);
+  if (pitch_bytes) *pitch_bytes = s->pitch * (int64_t)s->esz;
+  return RD_OK;
+}
+
+int rd_set_profiling(rd_sim* s, int32_t on) {
+  if (!s) return RD_EINVAL;
+  s->profiling = on != 0;
+  return RD_OK;
+}
+
+int rd_get_stats(rd_sim* s, rd_stats* out) {
+  if (!s || !out) return RD_EINVAL;
+  if (s->ev_used) {
+    RD_CUDA(s, cudaStreamSynchronize(s->stream));
+    for (size_t i = 0; i < s->ev_used; ++i) {
+      float ms = 0;
+      RD_CUDA(s, cudaEventElapsedTime(&ms, s->ev_pool[i].first, s->ev_pool[i].second));
+      s->acc_ms += ms;
+    }
+    s->acc_timed += (int64_t)s->ev_used;
+    s->ev_used = 0;
+  }
+  *out = s->st;
+  out->step_kernel_ms = s->acc_ms;
+  out->timed_launches = s->acc_timed;
+  out->tb_depth = s->K;
+  return RD_OK;
+}
+
+int rd_reset_stats(rd_sim* s) {
+  if (!s) return RD_EINVAL;
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  s->st = rd_stats{};
+  s->acc_ms = 0;
+  s->acc_timed = 0;
+  s->ev_used = 0;
+  return RD_OK;
+}
+
+}  // extern "C"

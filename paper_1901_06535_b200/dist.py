@@ -1,0 +1,203 @@
+"""Row-slab domain decomposition across GPUs.
+
+Rank r of G owns global rows [r*H/G, (r+1)*H/G) and all W columns, with
+`halo` ghost rows above and below (halo >= temporal-blocking depth k). After
+every rd_step(k) (k <= halo) the slab edges are exchanged with rank +-1:
+the owned top `halo` rows of u and v go to rank-1's bottom ghosts, the owned
+bottom rows to rank+1's top ghosts. Global top/bottom edges use the no-flux
+clamp inside the kernel, so the decomposition is bitwise invisible: the
+G-slab result equals the single-grid result (tests/test_dist_*).
+
+torch.distributed is the plumbing (process group; NCCL on B200, gloo in the
+CPU tests); the data path is device-to-device send/recv of contiguous row
+blocks straight out of the engine's planes. Inputs are generated in global
+coordinates (rdinputs), so they do not depend on G.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import rd_create_slab, rd_destroy, rd_get_stats, rd_probe_latch, rd_probe_result, rd_read_fields
+from . import rd_row_ptr, rd_set_stream, rd_step, rd_stimulate, rd_write_fields
+
+
+def slab_rows(H: int, world: int, rank: int) -> tuple[int, int]:
+    """(row0, rows) of rank's slab; H need not divide evenly (first H % G
+    ranks get one extra row)."""
+    base, extra = divmod(H, world)
+    row0 = rank * base + min(rank, extra)
+    return row0, base + (1 if rank < extra else 0)
+
+
+def ghost_extent(H: int, row0: int, rows: int, halo: int) -> tuple[int, int]:
+    """Global rows [lo, hi) a slab stores (owned + ghosts that exist)."""
+    return max(0, row0 - halo), min(H, row0 + rows + halo)
+
+
+def exchange_plan(world: int, rank: int, rows: int, halo: int):
+    """The (peer, local send rows, local recv rows) pairs of one exchange.
+    Local row x of a slab is global row row0 + x; ghosts are x < 0, x >= rows."""
+    plan = []
+    if rank > 0:
+        plan.append((rank - 1, (0, halo), (-halo, 0)))
+    if rank < world - 1:
+        plan.append((rank + 1, (rows - halo, rows), (rows, rows + halo)))
+    return plan
+
+
+def exchange(tensors_by_peer, group=None):
+    """One halo exchange: tensors_by_peer = [(peer, [send...], [recv...])].
+    All sends/recvs are posted as one batch (NCCL group) and waited on."""
+    import torch.distributed as dist
+    ops = []
+    for peer, sends, recvs in tensors_by_peer:
+        for s in sends:
+            ops.append(dist.P2POp(dist.isend, s, peer, group))
+        for r in recvs:
+            ops.append(dist.P2POp(dist.irecv, r, peer, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+class _DevRows:
+    """A contiguous device byte range as a __cuda_array_interface__ object."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+
+def _dev_rows(h, b: int, plane: int, r0: int, r1: int):
+    import torch
+    ptr, pitch = rd_row_ptr(h, b, plane, r0)
+    return torch.as_tensor(_DevRows(ptr, pitch * (r1 - r0)), device="cuda")
+
+
+class SlabSim:
+    """One rank's slab of a (batch of) grid(s), stepped with halo exchanges.
+
+    transport: "dist" (torch.distributed process group) or a LoopbackGroup
+    shared by several SlabSims on one device (virtual ranks for testing).
+    """
+
+    def __init__(self, W: int, H: int, rank: int, world: int, phi_fn, *, dtype=np.float32, halo: int = 4,
+                 tb_depth: int = 0, batch: int = 1, transport="dist", group=None, params=None, flags: int = 0):
+        self.W, self.H, self.rank, self.world, self.halo = W, H, rank, world, halo
+        self.row0, self.rows = slab_rows(H, world, rank)
+        if self.rows < halo and world > 1:
+            raise ValueError("slab thinner than the halo")
+        lo, hi = ghost_extent(H, self.row0, self.rows, halo)
+        phi = np.stack([np.ascontiguousarray(phi_fn(b, lo, hi - lo), dtype=dtype) for b in range(batch)])
+        self.dtype = np.dtype(dtype)
+        self.batch = batch
+        self.h = rd_create_slab(W, self.rows, phi, self.row0, H, halo, batch=batch, dtype=dtype,
+                                tb_depth=tb_depth or halo, flags=flags, params=params)
+        self.transport = transport
+        self.group = group
+        self.plan = exchange_plan(world, rank, self.rows, halo)
+        if not isinstance(transport, str):
+            transport.register(self)
+        else:
+            import torch
+            # NCCL work is ordered against torch's current stream: issue the
+            # engine's kernels on that stream too.
+            self.set_stream(torch.cuda.current_stream())
+
+    def close(self):
+        if self.h:
+            rd_destroy(self.h)
+            self.h = None
+
+    def set_stream(self, stream):
+        rd_set_stream(self.h, getattr(stream, "cuda_stream", stream))
+
+    def write(self, b: int, u_fn, v_fn=None):
+        """Write owned rows from global-row generators u_fn(b, row0, rows)."""
+        u = np.ascontiguousarray(u_fn(b, self.row0, self.rows), dtype=self.dtype)
+        v = None if v_fn is None else np.ascontiguousarray(v_fn(b, self.row0, self.rows), dtype=self.dtype)
+        rd_write_fields(self.h, b, u, v)
+
+    def stimulate(self, shape: dict, value: float = 1.0, at_step: int = 0, b: int = -1):
+        rd_stimulate(self.h, b, shape, value, at_step)  # global coordinates; the slab clips
+
+    def probe_latch(self, b, rect, threshold=0.1, stride=50):
+        return rd_probe_latch(self.h, b, rect, threshold, stride)
+
+    def probe_result(self, pid):
+        return rd_probe_result(self.h, pid)
+
+    def device_tensors(self, b: int):
+        """[(peer, [send u, send v], [recv u, recv v])] for the current buffers."""
+        out = []
+        for peer, (s0, s1), (r0, r1) in self.plan:
+            sends = [_dev_rows(self.h, b, p, s0, s1) for p in (0, 1)]
+            recvs = [_dev_rows(self.h, b, p, r0, r1) for p in (0, 1)]
+            out.append((peer, sends, recvs))
+        return out
+
+    def exchange(self):
+        if self.world == 1:
+            return
+        if isinstance(self.transport, str):
+            for b in range(self.batch):
+                exchange(self.device_tensors(b), self.group)
+        else:
+            self.transport.exchange(self)
+
+    def step(self, n: int):
+        """Advance n steps: blocks of <= halo steps, each preceded by a halo
+        exchange (so ghosts are fresh after writes, too)."""
+        while n > 0:
+            k = min(self.halo, n)
+            self.exchange()
+            rd_step(self.h, k)
+            n -= k
+
+    def read_owned(self, b: int = 0):
+        u = np.empty((self.rows, self.W), dtype=self.dtype)
+        v = np.empty((self.rows, self.W), dtype=self.dtype)
+        rd_read_fields(self.h, b, u, v)
+        return u, v
+
+    def stats(self):
+        return rd_get_stats(self.h)
+
+
+class LoopbackGroup:
+    """Virtual ranks on ONE device: an exchange is a set of device-to-device
+    copies between the registered slabs (no kernel ever waits on another), run
+    once every slab has finished its block. Used to test the decomposition
+    bitwise on a single GPU."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.slabs = {}
+        self.arrived = set()
+
+    def register(self, slab: SlabSim):
+        self.slabs[slab.rank] = slab
+
+    def exchange(self, slab: SlabSim):
+        self.arrived.add(slab.rank)
+        if len(self.arrived) < self.world:
+            return
+        self.arrived.clear()
+        for b in range(self.slabs[0].batch):
+            views = {r: dict((peer, (s, rv)) for peer, s, rv in sl.device_tensors(b)) for r, sl in self.slabs.items()}
+            for r, peers in views.items():
+                for peer, (sends, _) in peers.items():
+                    _, recvs = views[peer][r]
+                    for s, rv in zip(sends, recvs):
+                        rv.copy_(s)
+        import torch
+        torch.cuda.synchronize()  # the engine's streams are non-blocking
+
+    def step_all(self, n: int):
+        halo = self.slabs[0].halo
+        while n > 0:
+            k = min(halo, n)
+            for r in range(self.world):
+                self.slabs[r].exchange()
+            for r in range(self.world):
+                rd_step(self.slabs[r].h, k)
+            n -= k

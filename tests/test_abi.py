@@ -1,0 +1,85 @@
+"""The C-ABI library (no GPU needed): it loads, exports every symbol
+include/rd.h declares, matches the Python declarations, and validates
+arguments before touching the device."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1901_06535_b200 as rd
+from paper_1901_06535_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rd.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rd_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = header_functions()
+    assert len(names) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (rd_\w+)", out))
+    for n in names:
+        assert n in exported, n
+        assert getattr(lib, n) is not None
+    assert sorted(n for n, _, _ in _lib.SYMBOLS) == names
+
+
+def test_struct_layouts_match_header():
+    """Sizes of the ABI structs as a C compiler lays them out."""
+    code = r'''
+#include <stdio.h>
+#include "rd.h"
+int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(rd_params), sizeof(rd_grid), sizeof(rd_shape),
+ sizeof(rd_rect), sizeof(rd_fault), sizeof(rd_stats));return 0;}
+'''
+    exe = "/tmp/rd_sizes"
+    subprocess.run(["gcc", "-x", "c", "-I", os.path.join(ROOT, "include"), "-o", exe, "-"], input=code, text=True,
+                   check=True)
+    sizes = list(map(int, subprocess.run([exe], capture_output=True, text=True).stdout.split()))
+    ours = [C.sizeof(t) for t in (_lib.rd_params, _lib.rd_grid, _lib.rd_shape, _lib.rd_rect, _lib.rd_fault,
+                                  _lib.rd_stats)]
+    assert sizes == ours
+
+
+def test_abi_version_and_defaults(table1):
+    assert _lib.load().rd_abi_version() == 1
+    p = rd.rd_params_default()
+    for k in ("eps", "f", "q", "Du", "dt", "dx"):
+        assert getattr(p, k) == table1[k]
+
+
+@pytest.mark.parametrize("field,value", [("eps", 0.0), ("q", 1.5), ("dt", -1.0), ("dt", 0.04), ("f", float("nan"))])
+def test_param_validation_before_device(field, value):
+    """SPEC.md:28 invariants are rejected with RD_EPARAM (no device needed);
+    dt=0.04 violates dt*Du/dx^2 < 0.25."""
+    p = rd.rd_params_default()
+    setattr(p, field, value)
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create(8, 8, np.zeros((8, 8), np.float32), params=p)
+    assert e.value.code == _lib.RD_EPARAM
+
+
+def test_dims_validation_before_device():
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create(2, 8, np.zeros((8, 2), np.float32))
+    assert e.value.code == _lib.RD_EINVAL
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create(8, 8, np.zeros((8, 8), np.float32), tb_depth=99)
+    assert e.value.code == _lib.RD_EINVAL
+
+
+def test_no_cpu_fallback(monkeypatch, tmp_path):
+    """The product path fails loudly when the CUDA extension is missing."""
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(RuntimeError, match="not built"):
+        _lib.load(str(tmp_path / "missing.so"))

@@ -1,0 +1,83 @@
+"""GPU parity on the BASELINE.json configurations 2-5.
+
+Configs 2/3 (the paper's AND gate and diode shapes, §4) run in full
+(20000 steps) in fp32 and fp64, bitwise against the oracle, with the paper's
+outcomes. Configs 4/5 run at full size in the launch configuration bench.py
+times: bitwise vs the oracle over the first steps of the full grid, and by
+properties (blocking-depth invariance, determinism, boundedness) at full
+length where the oracle cannot follow.
+"""
+import numpy as np
+import pytest
+
+from gpu_util import assert_bitwise, gpu_run, oracle_run
+from helpers import golden
+from rdinputs import config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
+def test_and_gate_batched_truth_table(dtype):
+    """configs[1]: 4 truth-table rows in one batched launch; fields and probe
+    latches bitwise equal to the oracle; output fires only for 11
+    (PAPER.md:280-285)."""
+    w = config(2, dtype=dtype)
+    U, V, fire, _ = gpu_run(w)
+    expect = golden("paper_outcomes.json")["and_gate"]["fires"]
+    assert [f[0] >= 0 for f in fire] == expect
+    for b in range(w.B):
+        r = oracle_run(w, b)
+        assert fire[b] == r.first_fire
+        assert_bitwise(U[b], r.u, f"u row {b}")
+        assert_bitwise(V[b], r.v, f"v row {b}")
+    assert np.array_equal(U[1], U[2][:, ::-1])  # P-10 mirror symmetry
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
+def test_diode_batched(dtype):
+    """configs[2]: both directions in one batched launch; anode->cathode
+    crosses, cathode->anode does not."""
+    w = config(3, dtype=dtype)
+    U, V, fire, _ = gpu_run(w)
+    assert [f[0] >= 0 for f in fire] == golden("paper_outcomes.json")["diode"]["fires"]
+    for b in range(w.B):
+        r = oracle_run(w, b)
+        assert fire[b] == r.first_fire
+        assert_bitwise(U[b], r.u, f"u run {b}")
+        assert_bitwise(V[b], r.v, f"v run {b}")
+
+
+def test_config4_full_grid_first_steps_bitwise():
+    """configs[3] at full size (16384^2 fp32, noise + 64 half-discs) in the
+    bench launch configuration: the first 20 steps equal the oracle bitwise
+    on every cell of the full grid."""
+    w = config(4, steps=20)
+    U, V, _, st = gpu_run(w)
+    assert st["tb_depth"] >= 1
+    r = oracle_run(w, 0)
+    assert_bitwise(U[0], r.u, "u")
+    assert_bitwise(V[0], r.v, "v")
+
+
+def test_config4_full_length_properties():
+    """configs[3] for the full 10000 steps: blocking depth 1 and the auto
+    depth give bit-identical fields (T2), reruns are identical, and the
+    fields are finite and bounded."""
+    w = config(4)
+    Ua, Va, _, _ = gpu_run(w)
+    Ub, Vb, _, _ = gpu_run(w, tb_depth=1)
+    assert_bitwise(Ua, Ub, "u auto vs k=1")
+    assert_bitwise(Va, Vb, "v auto vs k=1")
+    assert np.isfinite(Ua).all() and np.isfinite(Va).all()
+    assert Ua.min() > -0.1 and Ua.max() < 1.1
+
+
+def test_config5_crop_bitwise():
+    """configs[4] inputs (noise, 256 obstacles of phi=0.2, masked half-discs)
+    on a 4096^2 crop of the global grid, 40 steps, bitwise vs the oracle."""
+    w = config(5, H=4096, W=4096, steps=40, n_obstacles=16)
+    U, V, _, _ = gpu_run(w)
+    r = oracle_run(w, 0)
+    assert_bitwise(U[0], r.u, "u")
+    assert_bitwise(V[0], r.v, "v")

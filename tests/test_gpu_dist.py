@@ -1,0 +1,62 @@
+"""Row-slab decomposition on ONE GPU with virtual ranks (LoopbackGroup): the
+G-slab result (kernels clamp only at global edges, ghosts come from the
+neighbour slab) is bitwise identical to the single-grid result and to the
+oracle (SURVEY.md §8(e) invariant)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1901_06535_b200 as rd
+from gpu_util import assert_bitwise
+from paper_1901_06535_b200.dist import LoopbackGroup, SlabSim
+from rdinputs import half_discs, noise_plane, obstacles
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("G,halo", [(2, 1), (2, 4), (3, 4), (4, 8)])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
+def test_virtual_slabs_equal_single_grid(G, halo, dtype):
+    H, W, steps = 203, 300, 37
+    rects = obstacles(H, W, 6, seed=3)
+
+    def phi_fn(b, row0, rows):
+        p = np.full((rows, W), 0.054)
+        for (y0, x0, y1, x1) in rects:
+            a, c = max(y0, row0), min(y1, row0 + rows)
+            if a < c:
+                p[a - row0:c - row0, x0:x1] = 0.2
+        return p
+
+    def u_fn(b, row0, rows):
+        return noise_plane(rows, W, 0, seed=1, dtype=dtype, row0=row0)
+
+    def v_fn(b, row0, rows):
+        return noise_plane(rows, W, 1, seed=1, dtype=dtype, row0=row0)
+
+    shapes = half_discs(H, W, 12, seed=2, mask_phi=0.054)
+    grp = LoopbackGroup(G)
+    slabs = [SlabSim(W, H, r, G, phi_fn, dtype=dtype, halo=halo, transport=grp) for r in range(G)]
+    for s in slabs:
+        s.write(0, u_fn, v_fn)
+        for sh in shapes:
+            s.stimulate(sh, 1.0, 0)
+        s.stimulate({"kind": "rect", "y0": 60, "x0": 10, "y1": 150, "x1": 14}, 1.0, 5)
+    grp.step_all(steps)
+    U = np.concatenate([s.read_owned(0)[0] for s in slabs])
+    V = np.concatenate([s.read_owned(0)[1] for s in slabs])
+    for s in slabs:
+        s.close()
+
+    ev = [(sh, 1.0, 0) for sh in shapes] + [({"kind": "rect", "y0": 60, "x0": 10, "y1": 150, "x1": 14}, 1.0, 5)]
+    ref = oracle.run(u_fn(0, 0, H), v_fn(0, 0, H), phi_fn(0, 0, H).astype(dtype), steps, events=ev)
+    assert_bitwise(U, ref.u, "u")
+    assert_bitwise(V, ref.v, "v")
+    sim = rd.Sim(phi_fn(0, 0, H).astype(dtype), dtype=dtype)
+    sim.write(0, u_fn(0, 0, H), v_fn(0, 0, H))
+    for (sh, val, at) in ev:
+        sim.stimulate(sh, val, at)
+    sim.step(steps)
+    u1, v1 = sim.read(0)
+    sim.close()
+    assert_bitwise(U, u1, "u single")
