@@ -131,6 +131,7 @@ typedef struct {
   int64_t timed_launches;  /* stencil launches covered by step_kernel_ms */
   int32_t tb_depth;        /* temporal-blocking depth in use */
   int32_t pad;
+  int64_t replays;         /* rd_step calls replayed from the checkpoint (fault or fast-division guard) */
 } rd_stats;
 
 /* ---- lifecycle ---- */

@@ -44,6 +44,7 @@ struct rd_sim {
   rd_params p{};
   size_t esz = 4;
   int64_t H = 0, W = 0, B = 0, pitch = 0, halo = 0, rows_alloc = 0, plane_stride = 0;
+  int64_t row_off = 0;  // halo + guard rows: element row offset of local row 0
   int64_t grow0 = 0, Hg = 0;
   bool slab = false;
   int top_edge = 1, bot_edge = 1;
@@ -55,6 +56,7 @@ struct rd_sim {
   void* ck_v = nullptr;
   int cur = 0;
   int64_t step = 0;
+  int32_t ghost_valid = 0;  // slab: ghost rows still valid in the current buffers
   int K = 4;
   std::vector<PendingEvent> events;
   std::vector<LatchedProbe> probes;
@@ -63,7 +65,9 @@ struct rd_sim {
   long long* d_first_ck = nullptr;
   int probes_cap = 0;
   bool probes_dirty = false;
-  unsigned long long* d_fault = nullptr;
+  unsigned long long* d_fault = nullptr;  // [0] fault key, [1] (as int) precise flag
+  int* d_precise = nullptr;
+  bool precise_mode = false;
   int* d_flag = nullptr;
   void* d_scratch = nullptr;  // probe max output
   cudaStream_t own_stream = nullptr;
@@ -157,7 +161,7 @@ int pick_hb(const rd_sim* s, int n_strips) {
   return (int)hb;
 }
 
-template <typename T, int K, bool REACT>
+template <typename T, int K, bool REACT, bool PRECISE>
 cudaError_t launch_tb_t(rd_sim* s, int in, int out) {
   constexpr int V = vec_of<T>();
   using G = rdk::StripGeom<K, V>;
@@ -174,6 +178,11 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out) {
   a.halo = (int32_t)s->halo;
   a.r_lo = s->r_lo;
   a.r_hi = s->r_hi;
+  // rows to produce: owned rows, plus at interior slab edges the ghost rows
+  // that stay valid for later launches of this rd_step (ghost depth g - k)
+  const int32_t keep = s->ghost_valid - K;
+  a.out_lo = s->top_edge ? 0 : -keep;
+  a.out_hi = (int32_t)s->H + (s->bot_edge ? 0 : keep);
   a.top_edge = s->top_edge;
   a.bot_edge = s->bot_edge;
   a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
@@ -182,29 +191,33 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out) {
   a.H_global = s->Hg;
   a.k = make_consts<T>(s->p);
   a.fault_key = s->d_fault;
+  a.precise_flag = s->d_precise;
   const int warps = 4;
-  dim3 grid((a.n_strips + warps - 1) / warps, (unsigned)((s->H + a.hb - 1) / a.hb), (unsigned)s->B);
-  rdk::tb_kernel<T, K, V, REACT><<<grid, warps * 32, 0, s->stream>>>(a);
+  const int64_t out_rows = a.out_hi - a.out_lo;
+  dim3 grid((a.n_strips + warps - 1) / warps, (unsigned)((out_rows + a.hb - 1) / a.hb), (unsigned)s->B);
+  rdk::tb_kernel<T, K, V, REACT, PRECISE><<<grid, warps * 32, 0, s->stream>>>(a);
   return cudaGetLastError();
 }
 
-template <typename T, bool REACT>
+template <typename T, bool REACT, bool PRECISE>
 cudaError_t launch_tb_k(rd_sim* s, int k, int in, int out) {
   switch (k) {
-    case 1: return launch_tb_t<T, 1, REACT>(s, in, out);
-    case 2: return launch_tb_t<T, 2, REACT>(s, in, out);
-    case 3: return launch_tb_t<T, 3, REACT>(s, in, out);
-    case 4: return launch_tb_t<T, 4, REACT>(s, in, out);
-    case 5: return launch_tb_t<T, 5, REACT>(s, in, out);
-    case 6: return launch_tb_t<T, 6, REACT>(s, in, out);
-    case 7: return launch_tb_t<T, 7, REACT>(s, in, out);
-    case 8: return launch_tb_t<T, 8, REACT>(s, in, out);
+    case 1: return launch_tb_t<T, 1, REACT, PRECISE>(s, in, out);
+    case 2: return launch_tb_t<T, 2, REACT, PRECISE>(s, in, out);
+    case 3: return launch_tb_t<T, 3, REACT, PRECISE>(s, in, out);
+    case 4: return launch_tb_t<T, 4, REACT, PRECISE>(s, in, out);
+    case 5: return launch_tb_t<T, 5, REACT, PRECISE>(s, in, out);
+    case 6: return launch_tb_t<T, 6, REACT, PRECISE>(s, in, out);
+    case 7: return launch_tb_t<T, 7, REACT, PRECISE>(s, in, out);
+    case 8: return launch_tb_t<T, 8, REACT, PRECISE>(s, in, out);
   }
   return cudaErrorInvalidValue;
 }
 
 int launch_tb(rd_sim* s, int k) {
   const int in = s->cur, out = s->cur ^ 1;
+  if (s->slab && k > s->ghost_valid)
+    return set_err(s, RD_ERANGE, "slab ghost rows exhausted (k=%d > %d valid rows)", k, s->ghost_valid);
   const bool react = !(s->g.flags & RD_REACTION_OFF);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (s->profiling) {
@@ -220,13 +233,21 @@ int launch_tb(rd_sim* s, int k) {
     RD_CUDA(s, cudaEventRecord(e0, s->stream));
   }
   cudaError_t e;
-  if (s->esz == 4)
-    e = react ? launch_tb_k<float, true>(s, k, in, out) : launch_tb_k<float, false>(s, k, in, out);
-  else
-    e = react ? launch_tb_k<double, true>(s, k, in, out) : launch_tb_k<double, false>(s, k, in, out);
+  // fp32 uses the fast-division kernels unless this is a precise replay (or
+  // no checkpoint exists to replay from); fp64 always divides with __ddiv_rn
+  const bool precise = s->precise_mode || (s->g.flags & RD_NO_CHECKPOINT);
+  if (s->esz == 4) {
+    if (!react)
+      e = launch_tb_k<float, false, true>(s, k, in, out);
+    else
+      e = precise ? launch_tb_k<float, true, true>(s, k, in, out) : launch_tb_k<float, true, false>(s, k, in, out);
+  } else {
+    e = react ? launch_tb_k<double, true, true>(s, k, in, out) : launch_tb_k<double, false, true>(s, k, in, out);
+  }
   if (e != cudaSuccess) return set_err(s, RD_ECUDA, "tb_kernel<k=%d> launch: %s", k, cudaGetErrorString(e));
   if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
   s->cur = out;
+  s->ghost_valid -= k;
   s->st.launches++;
   s->st.step_launches++;
   s->st.cell_updates += s->B * s->H * s->W * (int64_t)k;
@@ -266,11 +287,11 @@ int apply_event(rd_sim* s, const PendingEvent& ev) {
   dim3 grid((unsigned)((j1 - j0 + 127) / 128), (unsigned)(x1 - x0), (unsigned)nb);
   if (s->esz == 4)
     rdk::stamp_kernel<float><<<grid, block, 0, s->stream>>>(
-        (float*)s->u[s->cur], (const float*)s->phi, s->plane_stride, s->pitch, (int32_t)s->halo, s->grow0,
+        (float*)s->u[s->cur], (const float*)s->phi, s->plane_stride, s->pitch, (int32_t)s->row_off, s->grow0,
         ev.shape, (float)ev.value, (float)ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
   else
     rdk::stamp_kernel<double><<<grid, block, 0, s->stream>>>(
-        (double*)s->u[s->cur], (const double*)s->phi, s->plane_stride, s->pitch, (int32_t)s->halo, s->grow0,
+        (double*)s->u[s->cur], (const double*)s->phi, s->plane_stride, s->pitch, (int32_t)s->row_off, s->grow0,
         ev.shape, ev.value, ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
   RD_CUDA(s, cudaGetLastError());
   s->st.launches++;
@@ -325,11 +346,11 @@ int launch_probes(rd_sim* s, int64_t step) {
   if (!n) return RD_OK;
   if (s->esz == 4)
     rdk::probe_kernel<float><<<n, 256, 0, s->stream>>>((const float*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                        (int32_t)s->halo, s->d_probes, n, step, s->d_first,
+                                                        (int32_t)s->row_off, s->d_probes, n, step, s->d_first,
                                                         nullptr);
   else
     rdk::probe_kernel<double><<<n, 256, 0, s->stream>>>((const double*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                         (int32_t)s->halo, s->d_probes, n, step, s->d_first,
+                                                         (int32_t)s->row_off, s->d_probes, n, step, s->d_first,
                                                          nullptr);
   RD_CUDA(s, cudaGetLastError());
   s->st.launches++;
@@ -372,14 +393,19 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
   return RD_OK;
 }
 
-int read_fault(rd_sim* s, unsigned long long* key) {
-  RD_CUDA(s, cudaMemcpyAsync(key, s->d_fault, sizeof(*key), cudaMemcpyDeviceToHost, s->stream));
+// Reads the fault key and the fast-division precise flag (one 16-byte D2H).
+int read_fault(rd_sim* s, unsigned long long* key, int* precise) {
+  unsigned long long h[2];
+  RD_CUDA(s, cudaMemcpyAsync(h, s->d_fault, sizeof h, cudaMemcpyDeviceToHost, s->stream));
   RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  *key = h[0];
+  if (precise) *precise = (int)(h[1] & 0xffffffffu);
   return RD_OK;
 }
 
 int reset_fault(rd_sim* s) {
   RD_CUDA(s, cudaMemsetAsync(s->d_fault, 0xff, sizeof(unsigned long long), s->stream));
+  RD_CUDA(s, cudaMemsetAsync(s->d_fault + 1, 0, sizeof(unsigned long long), s->stream));
   return RD_OK;
 }
 
@@ -394,7 +420,8 @@ int alloc_planes(rd_sim* s) {
     RD_CUDA(s, cudaMalloc(&s->ck_u, bytes));
     RD_CUDA(s, cudaMalloc(&s->ck_v, bytes));
   }
-  RD_CUDA(s, cudaMalloc(&s->d_fault, sizeof(unsigned long long)));
+  RD_CUDA(s, cudaMalloc(&s->d_fault, 2 * sizeof(unsigned long long)));
+  s->d_precise = reinterpret_cast<int*>(s->d_fault + 1);
   RD_CUDA(s, cudaMalloc(&s->d_flag, sizeof(int)));
   RD_CUDA(s, cudaMalloc(&s->d_scratch, 64));
   return reset_fault(s);
@@ -418,7 +445,7 @@ int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
 }
 
 char* plane_ptr(rd_sim* s, void* plane, int64_t b, int64_t local_row) {
-  return (char*)plane + ((size_t)b * s->plane_stride + (size_t)(local_row + s->halo) * s->pitch) * s->esz;
+  return (char*)plane + ((size_t)b * s->plane_stride + (size_t)(local_row + s->row_off) * s->pitch) * s->esz;
 }
 
 int create_common(const rd_grid* grid, const rd_params* params, const void* phi_host, int64_t row0,
@@ -459,8 +486,10 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   s->bot_edge = s->grow0 + s->H == s->Hg;
   s->r_lo = s->top_edge ? 0 : -(int32_t)s->halo;
   s->r_hi = s->bot_edge ? (int32_t)s->H : (int32_t)(s->H + s->halo);
-  s->rows_alloc = s->H + 2 * s->halo;
+  s->rows_alloc = s->H + 2 * s->halo + 2 * rdk::kGuardRows;
+  s->row_off = s->halo + rdk::kGuardRows;
   s->plane_stride = s->rows_alloc * s->pitch;
+  s->ghost_valid = (int32_t)s->halo;
   s->K = grid->tb_depth > 0 ? grid->tb_depth : auto_tb(s);
   if (slab && s->K > s->halo) s->K = (int)s->halo;
   s->st.tb_depth = s->K;
@@ -651,6 +680,8 @@ int rd_step(rd_sim* s, int64_t n) {
   if (n < 0) return set_err(s, RD_EINVAL, "n must be >= 0");
   if (s->slab && n > s->halo) return set_err(s, RD_ERANGE, "slab handles step at most halo=%lld steps per call", (long long)s->halo);
   if (n == 0) return RD_OK;
+  // slab contract: the caller refreshed the ghost rows before this call
+  s->ghost_valid = (int32_t)s->halo;
   const bool ckpt = !(s->g.flags & RD_NO_CHECKPOINT);
   const int64_t step0 = s->step;
   const int cur0 = s->cur;
@@ -668,13 +699,15 @@ int rd_step(rd_sim* s, int64_t n) {
   }
   if ((rc = run_range(s, step0 + n, s->K))) return rc;
   unsigned long long key = ~0ull;
-  if ((rc = read_fault(s, &key))) return rc;
-  if (key == ~0ull) return RD_OK;
+  int precise_hit = 0;
+  if ((rc = read_fault(s, &key, &precise_hit))) return rc;
+  if (key == ~0ull && !precise_hit) return RD_OK;
 
   if (ckpt) {
-    // Replay from the checkpoint one step per launch to find the first failing
-    // step exactly; the handle is left at that step (results are bitwise
-    // independent of the blocking depth, so the replay reproduces the run).
+    // Replay from the checkpoint with PRECISE (__fdiv_rn) kernels, one step
+    // per launch, checking for non-finite cells after every step: the handle
+    // ends at the first failing step (or at step0+n), bit-identical to a
+    // step-by-step exact run (results do not depend on the blocking depth).
     const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
     s->cur = cur0;
     RD_CUDA(s, cudaMemcpyAsync(s->u[s->cur], s->ck_u, bytes, cudaMemcpyDeviceToDevice, s->stream));
@@ -684,13 +717,24 @@ int rd_step(rd_sim* s, int64_t n) {
                                  cudaMemcpyDeviceToDevice, s->stream));
     s->events = events0;
     s->step = step0;
+    s->ghost_valid = (int32_t)s->halo;
     if ((rc = reset_fault(s))) return rc;
     key = ~0ull;
+    s->precise_mode = true;
+    s->st.replays++;
     while (s->step < step0 + n) {
-      if ((rc = run_range(s, s->step + 1, 1))) return rc;
-      if ((rc = read_fault(s, &key))) return rc;
+      if ((rc = run_range(s, s->step + 1, 1))) {
+        s->precise_mode = false;
+        return rc;
+      }
+      if ((rc = read_fault(s, &key, nullptr))) {
+        s->precise_mode = false;
+        return rc;
+      }
       if (key != ~0ull) break;
     }
+    s->precise_mode = false;
+    if (key == ~0ull) return RD_OK;
   }
   const unsigned long long W = (unsigned long long)s->W, Hg = (unsigned long long)s->Hg;
   s->fault.step = s->step;
@@ -725,7 +769,7 @@ int rd_probe(rd_sim* s, int32_t b, const rd_rect* r, double threshold, int32_t* 
   if (s->esz == 4) {
     float* mo = (float*)((char*)s->d_scratch + 48);
     rdk::probe_kernel<float><<<1, 256, 0, s->stream>>>((const float*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                        (int32_t)s->halo, dp, 1, s->step, nullptr, mo);
+                                                        (int32_t)s->row_off, dp, 1, s->step, nullptr, mo);
     RD_CUDA(s, cudaGetLastError());
     float h;
     RD_CUDA(s, cudaMemcpyAsync(&h, mo, sizeof h, cudaMemcpyDeviceToHost, s->stream));
@@ -735,7 +779,7 @@ int rd_probe(rd_sim* s, int32_t b, const rd_rect* r, double threshold, int32_t* 
   } else {
     double* mo = (double*)((char*)s->d_scratch + 48);
     rdk::probe_kernel<double><<<1, 256, 0, s->stream>>>((const double*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                         (int32_t)s->halo, dp, 1, s->step, nullptr, mo);
+                                                         (int32_t)s->row_off, dp, 1, s->step, nullptr, mo);
     RD_CUDA(s, cudaGetLastError());
     RD_CUDA(s, cudaMemcpyAsync(&m, mo, sizeof m, cudaMemcpyDeviceToHost, s->stream));
     RD_CUDA(s, cudaStreamSynchronize(s->stream));

@@ -203,3 +203,34 @@ def test_write_fields_rejects_nonfinite():
     with pytest.raises(rd.RDError) as e:
         rd.Sim(phi)
     assert e.value.code == rd.RD_ENONFINITE
+
+
+@pytest.mark.parametrize("tb", [1, 4])
+def test_fast_division_guard_replay(tb):
+    """Cells with C + q below 2^-60 in magnitude trip the fast-division guard:
+    the rd_step is replayed precisely from its checkpoint (stats.replays) and
+    the result equals the oracle bitwise (finite or at the first fault)."""
+    H, W = 24, 40
+    dtype = np.float32
+    q = np.float32(0.002)
+    u0 = noise_plane(H, W, 0, seed=9, dtype=dtype)
+    v0 = noise_plane(H, W, 1, seed=9, dtype=dtype)
+    # C = -q + tiny: b = C + q in (0, 2^-60); C exactly -q: b = 0
+    u0[5, 7] = np.nextafter(-q, np.float32(0))
+    u0[12, 30] = -q
+    phi = np.full((H, W), 0.054, dtype)
+    ref = oracle.run(u0, v0, phi, 6)
+    sim = rd.Sim(phi, dtype=dtype, tb_depth=tb)
+    sim.write(0, u0, v0)
+    try:
+        sim.step(6)
+        assert ref.status == 0
+    except rd.RDError as e:
+        assert e.code == rd.RD_ENONFINITE and ref.status == -4
+        st, b, i, j = sim.fault()
+        assert (st, i, j) == ref.fault
+    u, v = sim.read(0)
+    assert sim.stats()["replays"] >= 1
+    assert_bitwise(u, ref.u, "u")
+    assert_bitwise(v, ref.v, "v")
+    sim.close()
