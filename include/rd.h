@@ -212,9 +212,11 @@ int rd_probe_result(struct rd_sim* sim, int32_t id, int64_t* first_fire_step);
 int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi_slab, int64_t row0,
                    int64_t height_global, int32_t halo, struct rd_sim** out);
 
-/* Device pointer to local row `row` (-halo <= row < height + halo) of instance
- * b's CURRENT u (plane 0) or v (plane 1), and the row pitch in bytes. The
- * pointer is valid until the next rd_step (buffers ping-pong). */
+/* Device pointer to the storage of local row `row` (-halo <= row < height +
+ * halo) of instance b's CURRENT u (plane 0) or v (plane 1), and the row pitch
+ * in bytes. A row's storage (pitch bytes) holds its cells plus its mirrored
+ * ghost columns, so rows [r0, r1) are one contiguous (r1-r0)*pitch byte range
+ * (what a halo exchange sends). Valid until the next rd_step (ping-pong). */
 int rd_row_ptr(struct rd_sim* sim, int32_t b, int32_t plane, int64_t row, void** ptr, int64_t* pitch_bytes);
 
 /* ---- measurement ---- */

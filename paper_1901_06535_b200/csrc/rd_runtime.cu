@@ -44,7 +44,10 @@ struct rd_sim {
   rd_params p{};
   size_t esz = 4;
   int64_t H = 0, W = 0, B = 0, pitch = 0, halo = 0, rows_alloc = 0, plane_stride = 0;
-  int64_t row_off = 0;  // halo + guard rows: element row offset of local row 0
+  int64_t row_off = 0;  // margin + guard rows: row offset of local row 0
+  int64_t col_off = 0;  // mirrored ghost columns left of column 0
+  int32_t margin = 0;   // ghost rows above/below (slab halo or mirror margin)
+  int fast_mode = 0;    // rdk::MODE_FOLD when 1/dx^2 is a power of two, else MODE_PRECISE
   int64_t grow0 = 0, Hg = 0;
   bool slab = false;
   int top_edge = 1, bot_edge = 1;
@@ -70,6 +73,7 @@ struct rd_sim {
   bool precise_mode = false;
   int* d_flag = nullptr;
   void* d_scratch = nullptr;  // probe max output
+  int num_sms = 148;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   bool profiling = false;
@@ -132,6 +136,7 @@ rdk::Consts<T> make_consts(const rd_params& p) {
   k.du = (T)p.Du;
   k.dt = (T)p.dt;
   k.inv_dx2 = (T)(1.0 / (p.dx * p.dx));
+  k.du_fold = (T)((double)k.du * (double)k.inv_dx2);
   return k;
 }
 
@@ -153,63 +158,94 @@ int pick_hb(const rd_sim* s, int n_strips) {
     int hb = atoi(e);
     if (hb >= 1) return hb;
   }
-  const int64_t target_tasks = 148 * 24;
-  int64_t hb = (s->H * (int64_t)n_strips * s->B + target_tasks - 1) / target_tasks;
-  hb = std::max<int64_t>(hb, 16);
-  hb = std::min<int64_t>(hb, 512);
-  hb = (hb + 7) / 8 * 8;
+  // rows per warp task: long enough to amortise the 2K-row pipeline fill,
+  // short enough for >= ~6 tasks per resident warp (tail < a few %)
+  const int64_t resident_warps = (int64_t)s->num_sms * 16;
+  int64_t hb = (s->H * (int64_t)n_strips * s->B) / (resident_warps * 6);
+  hb = std::max<int64_t>(hb, 32);
+  hb = std::min<int64_t>(hb, 256);
   return (int)hb;
 }
 
-template <typename T, int K, bool REACT, bool PRECISE>
-cudaError_t launch_tb_t(rd_sim* s, int in, int out) {
+template <typename T>
+T* origin(const rd_sim* s, void* plane) {
+  return (T*)plane + s->row_off * s->pitch + s->col_off;
+}
+
+// Refresh the mirrored ghost margins (no-flux edges) of up to three planes:
+// ghost columns of rows [x_lo, x_hi) and, at global edges, the ghost rows.
+int launch_mirror(rd_sim* s, void* p0, void* p1, void* p2, int32_t x_lo, int32_t x_hi) {
+  const int nplanes = p2 ? 3 : (p1 ? 2 : 1);
+  const int64_t cells = (int64_t)(x_hi - x_lo + 2 * rdk::kMarginRows) * 2 * rdk::kMarginCols +
+                        (int64_t)2 * rdk::kMarginRows * s->W;
+  const unsigned bx = (unsigned)std::min<int64_t>((cells + 255) / 256, 4 * s->num_sms);
+  dim3 grid(bx, (unsigned)(nplanes * s->B));
+  if (s->esz == 4)
+    rdk::mirror_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, p0), p1 ? origin<float>(s, p1) : nullptr,
+                                                          p2 ? origin<float>(s, p2) : nullptr, s->plane_stride,
+                                                          s->pitch, (int32_t)s->H, (int32_t)s->W, x_lo, x_hi,
+                                                          s->top_edge, s->bot_edge, (int32_t)s->B);
+  else
+    rdk::mirror_kernel<double><<<grid, 256, 0, s->stream>>>(
+        origin<double>(s, p0), p1 ? origin<double>(s, p1) : nullptr, p2 ? origin<double>(s, p2) : nullptr,
+        s->plane_stride, s->pitch, (int32_t)s->H, (int32_t)s->W, x_lo, x_hi, s->top_edge, s->bot_edge,
+        (int32_t)s->B);
+  RD_CUDA(s, cudaGetLastError());
+  s->st.launches++;
+  return RD_OK;
+}
+
+template <typename T, int K, bool REACT, int MODE>
+cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_hi) {
   constexpr int V = vec_of<T>();
   using G = rdk::StripGeom<K, V>;
   rdk::TBArgs<T> a;
-  a.u_in = (const T*)s->u[in];
-  a.v_in = (const T*)s->v[in];
-  a.phi = (const T*)s->phi;
-  a.u_out = (T*)s->u[out];
-  a.v_out = (T*)s->v[out];
+  a.u_in = origin<T>(s, s->u[in]);
+  a.v_in = origin<T>(s, s->v[in]);
+  a.phi = origin<T>(s, s->phi);
+  a.u_out = origin<T>(s, s->u[out]);
+  a.v_out = origin<T>(s, s->v[out]);
   a.plane_stride = s->plane_stride;
   a.pitch = s->pitch;
   a.H = (int32_t)s->H;
   a.W = (int32_t)s->W;
-  a.halo = (int32_t)s->halo;
-  a.r_lo = s->r_lo;
-  a.r_hi = s->r_hi;
-  // rows to produce: owned rows, plus at interior slab edges the ghost rows
-  // that stay valid for later launches of this rd_step (ghost depth g - k)
-  const int32_t keep = s->ghost_valid - K;
-  a.out_lo = s->top_edge ? 0 : -keep;
-  a.out_hi = (int32_t)s->H + (s->bot_edge ? 0 : keep);
-  a.top_edge = s->top_edge;
-  a.bot_edge = s->bot_edge;
+  a.out_lo = out_lo;
+  a.out_hi = out_hi;
   a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
   a.hb = pick_hb(s, a.n_strips);
+  a.batch = (int32_t)s->B;
+  a.pad_ = 0;
   a.grow0 = s->grow0;
   a.H_global = s->Hg;
   a.k = make_consts<T>(s->p);
   a.fault_key = s->d_fault;
   a.precise_flag = s->d_precise;
-  const int warps = 4;
-  const int64_t out_rows = a.out_hi - a.out_lo;
-  dim3 grid((a.n_strips + warps - 1) / warps, (unsigned)((out_rows + a.hb - 1) / a.hb), (unsigned)s->B);
-  rdk::tb_kernel<T, K, V, REACT, PRECISE><<<grid, warps * 32, 0, s->stream>>>(a);
+  const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
+  // persistent grid of one-warp CTAs: as many as can be resident (occupancy
+  // API), capped by the number of tasks
+  static int per_sm = 0;
+  if (!per_sm) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdk::tb_kernel<T, K, V, REACT, MODE>, 32, 0) !=
+            cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+  }
+  const int64_t grid = std::min<int64_t>(tasks, (int64_t)s->num_sms * per_sm);
+  rdk::tb_kernel<T, K, V, REACT, MODE><<<(unsigned)grid, 32, 0, s->stream>>>(a);
   return cudaGetLastError();
 }
 
-template <typename T, bool REACT, bool PRECISE>
-cudaError_t launch_tb_k(rd_sim* s, int k, int in, int out) {
+template <typename T, bool REACT, int MODE>
+cudaError_t launch_tb_k(rd_sim* s, int k, int in, int out, int32_t lo, int32_t hi) {
   switch (k) {
-    case 1: return launch_tb_t<T, 1, REACT, PRECISE>(s, in, out);
-    case 2: return launch_tb_t<T, 2, REACT, PRECISE>(s, in, out);
-    case 3: return launch_tb_t<T, 3, REACT, PRECISE>(s, in, out);
-    case 4: return launch_tb_t<T, 4, REACT, PRECISE>(s, in, out);
-    case 5: return launch_tb_t<T, 5, REACT, PRECISE>(s, in, out);
-    case 6: return launch_tb_t<T, 6, REACT, PRECISE>(s, in, out);
-    case 7: return launch_tb_t<T, 7, REACT, PRECISE>(s, in, out);
-    case 8: return launch_tb_t<T, 8, REACT, PRECISE>(s, in, out);
+    case 1: return launch_tb_t<T, 1, REACT, MODE>(s, in, out, lo, hi);
+    case 2: return launch_tb_t<T, 2, REACT, MODE>(s, in, out, lo, hi);
+    case 3: return launch_tb_t<T, 3, REACT, MODE>(s, in, out, lo, hi);
+    case 4: return launch_tb_t<T, 4, REACT, MODE>(s, in, out, lo, hi);
+    case 5: return launch_tb_t<T, 5, REACT, MODE>(s, in, out, lo, hi);
+    case 6: return launch_tb_t<T, 6, REACT, MODE>(s, in, out, lo, hi);
+    case 7: return launch_tb_t<T, 7, REACT, MODE>(s, in, out, lo, hi);
+    case 8: return launch_tb_t<T, 8, REACT, MODE>(s, in, out, lo, hi);
   }
   return cudaErrorInvalidValue;
 }
@@ -232,22 +268,33 @@ int launch_tb(rd_sim* s, int k) {
     ++s->ev_used;
     RD_CUDA(s, cudaEventRecord(e0, s->stream));
   }
+  // rows to produce: owned rows, plus at interior slab edges the ghost rows
+  // that stay valid for later launches of this rd_step (ghost depth g - k)
+  const int32_t keep = s->slab ? s->ghost_valid - k : 0;
+  const int32_t lo = s->top_edge ? 0 : -keep;
+  const int32_t hi = (int32_t)s->H + (s->bot_edge ? 0 : keep);
   cudaError_t e;
-  // fp32 uses the fast-division kernels unless this is a precise replay (or
-  // no checkpoint exists to replay from); fp64 always divides with __ddiv_rn
-  const bool precise = s->precise_mode || (s->g.flags & RD_NO_CHECKPOINT);
+  // the fast modes (exact rewrites + guarded fp32 division) unless this is a
+  // precise replay or there is no checkpoint to replay from
+  const bool precise = s->precise_mode || (s->g.flags & RD_NO_CHECKPOINT) || s->fast_mode == rdk::MODE_PRECISE;
   if (s->esz == 4) {
     if (!react)
-      e = launch_tb_k<float, false, true>(s, k, in, out);
+      e = launch_tb_k<float, false, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
     else
-      e = precise ? launch_tb_k<float, true, true>(s, k, in, out) : launch_tb_k<float, true, false>(s, k, in, out);
+      e = precise ? launch_tb_k<float, true, rdk::MODE_PRECISE>(s, k, in, out, lo, hi)
+                  : launch_tb_k<float, true, rdk::MODE_FOLD>(s, k, in, out, lo, hi);
   } else {
-    e = react ? launch_tb_k<double, true, true>(s, k, in, out) : launch_tb_k<double, false, true>(s, k, in, out);
+    if (!react)
+      e = launch_tb_k<double, false, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
+    else
+      e = precise ? launch_tb_k<double, true, rdk::MODE_PRECISE>(s, k, in, out, lo, hi)
+                  : launch_tb_k<double, true, rdk::MODE_FOLD>(s, k, in, out, lo, hi);
   }
   if (e != cudaSuccess) return set_err(s, RD_ECUDA, "tb_kernel<k=%d> launch: %s", k, cudaGetErrorString(e));
   if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
   s->cur = out;
   s->ghost_valid -= k;
+  if (int rc = launch_mirror(s, s->u[out], s->v[out], nullptr, lo, hi)) return rc;
   s->st.launches++;
   s->st.step_launches++;
   s->st.cell_updates += s->B * s->H * s->W * (int64_t)k;
@@ -287,12 +334,12 @@ int apply_event(rd_sim* s, const PendingEvent& ev) {
   dim3 grid((unsigned)((j1 - j0 + 127) / 128), (unsigned)(x1 - x0), (unsigned)nb);
   if (s->esz == 4)
     rdk::stamp_kernel<float><<<grid, block, 0, s->stream>>>(
-        (float*)s->u[s->cur], (const float*)s->phi, s->plane_stride, s->pitch, (int32_t)s->row_off, s->grow0,
-        ev.shape, (float)ev.value, (float)ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
+        origin<float>(s, s->u[s->cur]), origin<float>(s, s->phi), s->plane_stride, s->pitch, s->grow0, ev.shape,
+        (float)ev.value, (float)ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
   else
     rdk::stamp_kernel<double><<<grid, block, 0, s->stream>>>(
-        (double*)s->u[s->cur], (const double*)s->phi, s->plane_stride, s->pitch, (int32_t)s->row_off, s->grow0,
-        ev.shape, ev.value, ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
+        origin<double>(s, s->u[s->cur]), origin<double>(s, s->phi), s->plane_stride, s->pitch, s->grow0, ev.shape,
+        ev.value, ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
   RD_CUDA(s, cudaGetLastError());
   s->st.launches++;
   return RD_OK;
@@ -345,13 +392,11 @@ int launch_probes(rd_sim* s, int64_t step) {
   const int n = (int)s->probes.size();
   if (!n) return RD_OK;
   if (s->esz == 4)
-    rdk::probe_kernel<float><<<n, 256, 0, s->stream>>>((const float*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                        (int32_t)s->row_off, s->d_probes, n, step, s->d_first,
-                                                        nullptr);
+    rdk::probe_kernel<float><<<n, 256, 0, s->stream>>>(origin<float>(s, s->u[s->cur]), s->plane_stride, s->pitch,
+                                                        s->d_probes, n, step, s->d_first, nullptr);
   else
-    rdk::probe_kernel<double><<<n, 256, 0, s->stream>>>((const double*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                         (int32_t)s->row_off, s->d_probes, n, step, s->d_first,
-                                                         nullptr);
+    rdk::probe_kernel<double><<<n, 256, 0, s->stream>>>(origin<double>(s, s->u[s->cur]), s->plane_stride, s->pitch,
+                                                         s->d_probes, n, step, s->d_first, nullptr);
   RD_CUDA(s, cudaGetLastError());
   s->st.launches++;
   return RD_OK;
@@ -368,15 +413,18 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
   int rc = sync_probes(s);
   if (rc) return rc;
   while (s->step < end) {
-    // a1: stimuli due now, in submission order
+    // a1: stimuli due now, in submission order; then refresh u's mirrors
+    bool stamped = false;
     for (size_t i = 0; i < s->events.size();) {
       if (s->events[i].at == s->step) {
         if ((rc = apply_event(s, s->events[i]))) return rc;
         s->events.erase(s->events.begin() + i);
+        stamped = true;
       } else {
         ++i;
       }
     }
+    if (stamped && (rc = launch_mirror(s, s->u[s->cur], nullptr, nullptr, s->r_lo, s->r_hi))) return rc;
     int64_t next = end;
     for (const auto& ev : s->events)
       if (ev.at > s->step) next = std::min(next, ev.at);
@@ -445,7 +493,8 @@ int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
 }
 
 char* plane_ptr(rd_sim* s, void* plane, int64_t b, int64_t local_row) {
-  return (char*)plane + ((size_t)b * s->plane_stride + (size_t)(local_row + s->row_off) * s->pitch) * s->esz;
+  return (char*)plane +
+         ((size_t)b * s->plane_stride + (size_t)(local_row + s->row_off) * s->pitch + (size_t)s->col_off) * s->esz;
 }
 
 int create_common(const rd_grid* grid, const rd_params* params, const void* phi_host, int64_t row0,
@@ -473,10 +522,13 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   s->H = grid->height;
   s->W = grid->width;
   s->B = grid->batch;
-  s->pitch = grid->pitch > 0 ? grid->pitch : (grid->width + 31) / 32 * 32;
-  if (s->pitch < s->W || s->pitch % 32) {
+  // columns: kMarginCols mirrored ghosts left and right, plus room for the
+  // last strip's lanes (shifted to a vector-aligned start)
+  const int64_t min_pitch = rdk::kMarginCols + grid->width + rdk::kMarginCols + 16;
+  s->pitch = grid->pitch > 0 ? grid->pitch : (min_pitch + 31) / 32 * 32;
+  if (s->pitch < min_pitch || s->pitch % 32) {
     delete s;
-    return set_err(nullptr, RD_EINVAL, "pitch must be >= width and a multiple of 32");
+    return set_err(nullptr, RD_EINVAL, "pitch must be a multiple of 32 and >= width + %d", (int)(min_pitch - grid->width));
   }
   s->slab = slab;
   s->halo = slab ? halo : 0;
@@ -486,9 +538,19 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   s->bot_edge = s->grow0 + s->H == s->Hg;
   s->r_lo = s->top_edge ? 0 : -(int32_t)s->halo;
   s->r_hi = s->bot_edge ? (int32_t)s->H : (int32_t)(s->H + s->halo);
-  s->rows_alloc = s->H + 2 * s->halo + 2 * rdk::kGuardRows;
-  s->row_off = s->halo + rdk::kGuardRows;
+  s->margin = (int32_t)std::max<int64_t>(s->halo, rdk::kMarginRows);
+  s->row_off = s->margin + rdk::kGuardRows;
+  s->col_off = rdk::kMarginCols;
+  s->rows_alloc = s->H + 2 * s->row_off;
   s->plane_stride = s->rows_alloc * s->pitch;
+  {
+    // Du may be folded into the Laplacian scale when 1/dx^2 is a power of two
+    // in the working precision (then du*(d*inv_dx2) == d*(du*inv_dx2) exactly)
+    const double inv = 1.0 / (params->dx * params->dx);
+    int ex = 0;
+    const double fr = std::frexp(inv, &ex);
+    s->fast_mode = (fr == 0.5 && ex > -100 && ex < 100) ? rdk::MODE_FOLD : rdk::MODE_PRECISE;
+  }
   s->ghost_valid = (int32_t)s->halo;
   s->K = grid->tb_depth > 0 ? grid->tb_depth : auto_tb(s);
   if (slab && s->K > s->halo) s->K = (int)s->halo;
@@ -505,6 +567,12 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
     return fail(RD_ECUDA);
   }
   s->stream = s->own_stream;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (s->num_sms < 1) s->num_sms = 148;
+  }
   if (int rc = alloc_planes(s)) return fail(rc);
   // phi rows present in the host buffer: local [lo, hi)
   const int64_t lo = slab ? std::max<int64_t>(0, row0 - halo) - row0 : 0;
@@ -524,6 +592,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
       return fail(RD_ENONFINITE);
     }
   }
+  if (int rc = launch_mirror(s, s->phi, s->u[0], s->v[0], s->r_lo, s->r_hi)) return fail(rc);
   if (cudaStreamSynchronize(s->stream) != cudaSuccess) {
     s->err = "stream sync failed";
     return fail(RD_ECUDA);
@@ -564,7 +633,8 @@ int write_fields(rd_sim* s, int32_t b, const void* u, const void* v, cudaMemcpyK
     if (int rc = check_finite_dev(s, plane_ptr(s, planes[k], b, 0), s->H, &bad)) return rc;
     if (bad) return set_err(s, RD_ENONFINITE, "rd_write_fields: %s contains non-finite values", k ? "v" : "u");
   }
-  return RD_OK;
+  return launch_mirror(s, u ? s->u[s->cur] : s->v[s->cur], (u && v) ? s->v[s->cur] : nullptr, nullptr, s->r_lo,
+                       s->r_hi);
 }
 
 }  // namespace
@@ -768,8 +838,8 @@ int rd_probe(rd_sim* s, int32_t b, const rd_rect* r, double threshold, int32_t* 
   double m = 0;
   if (s->esz == 4) {
     float* mo = (float*)((char*)s->d_scratch + 48);
-    rdk::probe_kernel<float><<<1, 256, 0, s->stream>>>((const float*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                        (int32_t)s->row_off, dp, 1, s->step, nullptr, mo);
+    rdk::probe_kernel<float><<<1, 256, 0, s->stream>>>(origin<float>(s, s->u[s->cur]), s->plane_stride, s->pitch,
+                                                        dp, 1, s->step, nullptr, mo);
     RD_CUDA(s, cudaGetLastError());
     float h;
     RD_CUDA(s, cudaMemcpyAsync(&h, mo, sizeof h, cudaMemcpyDeviceToHost, s->stream));
@@ -778,8 +848,8 @@ int rd_probe(rd_sim* s, int32_t b, const rd_rect* r, double threshold, int32_t* 
     if (fired) *fired = h >= (float)threshold;
   } else {
     double* mo = (double*)((char*)s->d_scratch + 48);
-    rdk::probe_kernel<double><<<1, 256, 0, s->stream>>>((const double*)s->u[s->cur], s->plane_stride, s->pitch,
-                                                         (int32_t)s->row_off, dp, 1, s->step, nullptr, mo);
+    rdk::probe_kernel<double><<<1, 256, 0, s->stream>>>(origin<double>(s, s->u[s->cur]), s->plane_stride, s->pitch,
+                                                         dp, 1, s->step, nullptr, mo);
     RD_CUDA(s, cudaGetLastError());
     RD_CUDA(s, cudaMemcpyAsync(&m, mo, sizeof m, cudaMemcpyDeviceToHost, s->stream));
     RD_CUDA(s, cudaStreamSynchronize(s->stream));
@@ -817,7 +887,9 @@ int rd_row_ptr(rd_sim* s, int32_t b, int32_t plane, int64_t row, void** ptr, int
   if (int rc = check_b(s, b)) return rc;
   if (plane != 0 && plane != 1) return set_err(s, RD_EINVAL, "plane must be 0 (u) or 1 (v)");
   if (row < -s->halo || row >= s->H + s->halo) return set_err(s, RD_ERANGE, "row %lld outside the slab", (long long)row);
-  *ptr = plane_ptr(s, plane == 0 ? s->u[s->cur] : s->v[s->cur], b, row);
+  // start of the row's storage (ghost columns included): a block of rows is
+  // a contiguous (rows x pitch) byte range
+  *ptr = plane_ptr(s, plane == 0 ? s->u[s->cur] : s->v[s->cur], b, row) - s->col_off * s->esz;
   if (pitch_bytes) *pitch_bytes = s->pitch * (int64_t)s->esz;
   return RD_OK;
 }
