@@ -153,18 +153,33 @@ constexpr int vec_of() {
   return 16 / (int)sizeof(T);
 }
 
-int pick_hb(const rd_sim* s, int n_strips) {
+// Rows per task. A task costs (hb + 2K) row iterations (the 2K-row pipeline
+// fill/drain is overhead); the persistent CTAs take tasks round-robin, so a
+// launch lasts ~ ceil(tasks / ctas) * (hb + 2K) row iterations, each taking
+// ~max(kLatencyWarps, warps resident per SM) issue-shares of the SM (a lone
+// warp is latency-bound; ~6 warps per SM saturate its issue slots). Pick the
+// hb minimising that: big grids get long tasks and no partial last wave,
+// small batched grids get short tasks spread over the whole chip.
+int pick_hb(const rd_sim* s, int n_strips, int64_t rows, int K, int64_t ctas) {
+  constexpr double kLatencyWarps = 6.0;
   if (const char* e = getenv("RD_HB")) {
     int hb = atoi(e);
     if (hb >= 1) return hb;
   }
-  // rows per warp task: long enough to amortise the 2K-row pipeline fill,
-  // short enough for >= ~6 tasks per resident warp (tail < a few %)
-  const int64_t resident_warps = (int64_t)s->num_sms * 16;
-  int64_t hb = (s->H * (int64_t)n_strips * s->B) / (resident_warps * 6);
-  hb = std::max<int64_t>(hb, 32);
-  hb = std::min<int64_t>(hb, 256);
-  return (int)hb;
+  int best = 1;
+  double best_cost = 1e300;
+  for (int hb = 1; hb <= 1024; ++hb) {
+    const int64_t tasks = (int64_t)n_strips * ((rows + hb - 1) / hb) * s->B;
+    const int64_t waves = (tasks + ctas - 1) / ctas;
+    const double per_sm = std::min<double>((double)ctas / s->num_sms, std::ceil((double)tasks / s->num_sms));
+    const double cost = (double)waves * (hb + 2 * K) * std::max(kLatencyWarps, per_sm) + 1e-9 * hb;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = hb;
+    }
+    if (hb >= rows) break;
+  }
+  return best;
 }
 
 template <typename T>
@@ -212,15 +227,6 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_
   a.out_lo = out_lo;
   a.out_hi = out_hi;
   a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
-  a.hb = pick_hb(s, a.n_strips);
-  a.batch = (int32_t)s->B;
-  a.pad_ = 0;
-  a.grow0 = s->grow0;
-  a.H_global = s->Hg;
-  a.k = make_consts<T>(s->p);
-  a.fault_key = s->d_fault;
-  a.precise_flag = s->d_precise;
-  const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
   // persistent grid of one-warp CTAs: as many as can be resident (occupancy
   // API), capped by the number of tasks
   static int per_sm = 0;
@@ -230,7 +236,17 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_
         per_sm < 1)
       per_sm = 1;
   }
-  const int64_t grid = std::min<int64_t>(tasks, (int64_t)s->num_sms * per_sm);
+  const int64_t ctas = (int64_t)s->num_sms * per_sm;
+  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, K, ctas);
+  a.batch = (int32_t)s->B;
+  a.pad_ = 0;
+  a.grow0 = s->grow0;
+  a.H_global = s->Hg;
+  a.k = make_consts<T>(s->p);
+  a.fault_key = s->d_fault;
+  a.precise_flag = s->d_precise;
+  const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
+  const int64_t grid = std::min<int64_t>(tasks, ctas);
   rdk::tb_kernel<T, K, V, REACT, MODE><<<(unsigned)grid, 32, 0, s->stream>>>(a);
   return cudaGetLastError();
 }

@@ -1,0 +1,75 @@
+#!/usr/bin/env python
+"""Throughput of the engine on every BASELINE.json configuration that fits one
+GPU (informational; bench.py is the contract line). For each config it runs
+the full configured step count through rd_step and reports device time,
+Gcell-updates/s, launches and the probe outcomes. Prints one JSON per config.
+
+  python scripts/bench_configs.py [--configs 1,2,3,4] [--dtype f32|f64|both]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1901_06535_b200 as rd  # noqa: E402
+from rdinputs import config  # noqa: E402
+
+
+def run(n, dtype, tb):
+    w = config(n, dtype=dtype)
+    phi = np.stack([w.phi_plane(b).astype(dtype) for b in range(w.B)])
+    sim = rd.Sim(phi, dtype=dtype, tb_depth=tb)
+    if w.init is not None:
+        for b in range(w.B):
+            u0, v0 = w.init_planes(b)
+            sim.write(b, u0, v0)
+    for b in range(w.B):
+        for shape, val, at in w.events[b]:
+            sim.stimulate(shape, val, at, b=b)
+    pids = [[sim.probe_latch(b, r, t, s) for (r, t, s) in w.probes[b]] for b in range(w.B)] if w.probes else []
+    stream = torch.cuda.current_stream()
+    sim.set_stream(stream)
+    rd.rd_reset_stats(sim.h)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    sim.step(w.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    st = sim.stats()
+    fires = [[sim.probe_result(p) for p in ps] for ps in pids]
+    cells = w.B * w.H * w.W * w.steps
+    sim.close()
+    return {"config": w.name, "dtype": np.dtype(dtype).name, "B": w.B, "H": w.H, "W": w.W, "steps": w.steps,
+            "device_ms": ms, "wall_s": wall, "gcell_updates_per_s": cells / (ms / 1e3) / 1e9,
+            "launches": st["launches"], "step_launches": st["step_launches"], "tb_depth": st["tb_depth"],
+            "first_fire": fires, "expect": w.expect.get("fires")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4")
+    ap.add_argument("--dtype", default="both")
+    ap.add_argument("--tb", type=int, default=0)
+    a = ap.parse_args()
+    dts = {"f32": [np.float32], "f64": [np.float64], "both": [np.float32, np.float64]}[a.dtype]
+    for n in map(int, a.configs.split(",")):
+        for dt in dts:
+            if n == 4 and dt == np.float64:
+                continue
+            print(json.dumps(run(n, dt, a.tb)), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,15 @@
+# Round profiling: default bench line, per-config throughput, ncu launch list of
+# the bench command, one ncu --set full capture of the top kernel.
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv,noheader > gpurun_out/gpu.txt
+python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench_default.log
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_reference.log
+python scripts/bench_configs.py > gpurun_out/bench_configs.log 2>&1; echo "configs rc=$?"; cat gpurun_out/bench_configs.log
+CMD="python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline"
+$CMD > gpurun_out/plain_list.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
+echo "launch list rc=$?"
+CMD2="python bench.py --timesteps 100 --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+$CMD2 > gpurun_out/plain_full.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:tb_kernel -s 20 -c 1 -o gpurun_out/prof_full $CMD2 > gpurun_out/ncu_full.log 2>&1
+echo "full rc=$?"

@@ -1,0 +1,105 @@
+#!/usr/bin/env python
+"""Summarise ncu outputs (gpurun_out/) into tracked files under profiles/.
+
+  python scripts/summarize_ncu.py --round r01 [--launches gpurun_out/launches.csv]
+                                   [--full gpurun_out/prof_full.ncu-rep]
+
+Writes profiles/<round>_launches.json (per-kernel launch count, total and
+average device time, share of the launch list) and
+profiles/<round>_<kernel>_full.json (the key --set full metrics of the top
+kernel: duration, DRAM bytes, throughput, occupancy, issue, stall reasons),
+plus profiles/traffic_<round>.json (dram bytes per launch) read by bench.py.
+"""
+import argparse
+import collections
+import csv
+import json
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROF = os.path.join(ROOT, "profiles")
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "launch__shared_mem_per_block_static", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+    "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+]
+
+
+def to_us(v, unit):
+    v = float(str(v).replace(",", ""))
+    return {"ns": v / 1e3, "nsecond": v / 1e3, "us": v, "usecond": v, "ms": v * 1e3, "msecond": v * 1e3}.get(unit, v)
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    hdr, data = rows[hi], rows[hi + 1:]
+    ki, mi, vi, ui = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    for r in data:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+            continue
+        name = r[ki].split("(")[0].replace("void ", "")
+        tot[name] += to_us(r[vi], r[ui])
+        cnt[name] += 1
+    T = sum(tot.values())
+    return [{"kernel": k, "launches": cnt[k], "total_ms": tot[k] / 1e3, "avg_us": tot[k] / cnt[k],
+             "share": tot[k] / T} for k in sorted(tot, key=lambda k: -tot[k])]
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {}
+    for h, u, v in zip(hdr, units, vals):
+        if h in KEYS:
+            d[h] = {"value": v, "unit": u}
+        if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+            try:
+                d.setdefault("stall_per_issue", {})[h[len("smsp__average_warps_issue_stalled_"):-len(
+                    "_per_issue_active.ratio")]] = float(v)
+            except ValueError:
+                pass
+    d["kernel"] = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--round", default="r01")
+    ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches.csv"))
+    ap.add_argument("--full", default=os.path.join(ROOT, "gpurun_out", "prof_full.ncu-rep"))
+    ap.add_argument("--cmd", default="")
+    a = ap.parse_args()
+    os.makedirs(PROF, exist_ok=True)
+    if os.path.exists(a.launches):
+        L = launches(a.launches)
+        json.dump({"source": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised: "
+                             "compare shares, not absolutes)", "command": a.cmd, "kernels": L},
+                  open(os.path.join(PROF, f"{a.round}_launches.json"), "w"), indent=1)
+        for r in L:
+            print(f"{r['kernel'][:70]:70s} n={r['launches']:5d} avg={r['avg_us']:10.1f} us share={r['share']*100:6.2f}%")
+    if os.path.exists(a.full):
+        F = full(a.full)
+        json.dump(F, open(os.path.join(PROF, f"{a.round}_tb_kernel_full.json"), "w"), indent=1)
+        rb = float(F["dram__bytes_read.sum"]["value"]) * (1e9 if F["dram__bytes_read.sum"]["unit"] == "Gbyte" else 1e6 if F["dram__bytes_read.sum"]["unit"] == "Mbyte" else 1)
+        wb = float(F["dram__bytes_write.sum"]["value"]) * (1e9 if F["dram__bytes_write.sum"]["unit"] == "Gbyte" else 1e6 if F["dram__bytes_write.sum"]["unit"] == "Mbyte" else 1)
+        json.dump({"kernel": F["kernel"], "dram_bytes_per_launch": rb + wb, "read": rb, "write": wb,
+                   "source": f"ncu --set full capture ({os.path.basename(a.full)})"},
+                  open(os.path.join(PROF, f"traffic_{a.round}.json"), "w"), indent=1)
+        for k, v in F.items():
+            print(k, v)
+
+
+if __name__ == "__main__":
+    main()
