@@ -132,6 +132,8 @@ typedef struct {
   int32_t tb_depth;        /* temporal-blocking depth in use */
   int32_t pad;
   int64_t replays;         /* rd_step calls replayed from the checkpoint (fault or fast-division guard) */
+  int32_t arith_mode;      /* 0 precise (canonical ops), 2 exact rewrites, 3 exact rewrites + certified 4-op fp32 division */
+  int32_t pad2;
 } rd_stats;
 
 /* ---- lifecycle ---- */

@@ -171,7 +171,7 @@ def rd_set_profiling(h, on: bool) -> None:
 def rd_get_stats(h) -> dict:
     s = _lib.rd_stats()
     _check(load().rd_get_stats(h, C.byref(s)), h)
-    return {k: getattr(s, k) for k, _ in s._fields_ if k != "pad"}
+    return {k: getattr(s, k) for k, _ in s._fields_ if not k.startswith("pad")}
 
 
 def rd_reset_stats(h) -> None:

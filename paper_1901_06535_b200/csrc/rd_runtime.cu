@@ -47,7 +47,8 @@ struct rd_sim {
   int64_t row_off = 0;  // margin + guard rows: row offset of local row 0
   int64_t col_off = 0;  // mirrored ghost columns left of column 0
   int32_t margin = 0;   // ghost rows above/below (slab halo or mirror margin)
-  int fast_mode = 0;    // rdk::MODE_FOLD when 1/dx^2 is a power of two, else MODE_PRECISE
+  int64_t div4_mismatches = -1;  // result of the 4-op division certification (-1: not run)
+  int fast_mode = 0;    // rdk::MODE_FOLD[_DIV4] when 1/dx^2 is a power of two, else MODE_PRECISE
   int64_t grow0 = 0, Hg = 0;
   bool slab = false;
   int top_edge = 1, bot_edge = 1;
@@ -296,9 +297,12 @@ int launch_tb(rd_sim* s, int k) {
   if (s->esz == 4) {
     if (!react)
       e = launch_tb_k<float, false, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
+    else if (precise)
+      e = launch_tb_k<float, true, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
+    else if (s->fast_mode == rdk::MODE_FOLD_DIV4)
+      e = launch_tb_k<float, true, rdk::MODE_FOLD_DIV4>(s, k, in, out, lo, hi);
     else
-      e = precise ? launch_tb_k<float, true, rdk::MODE_PRECISE>(s, k, in, out, lo, hi)
-                  : launch_tb_k<float, true, rdk::MODE_FOLD>(s, k, in, out, lo, hi);
+      e = launch_tb_k<float, true, rdk::MODE_FOLD>(s, k, in, out, lo, hi);
   } else {
     if (!react)
       e = launch_tb_k<double, false, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
@@ -508,6 +512,32 @@ int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
   return RD_OK;
 }
 
+// Enables the 4-op fp32 division if, for this handle's q, it equals IEEE
+// div.rn on every input the reaction can produce (exhaustive check of all
+// 2^32 fp32 values of C on the GPU, a few ms; cached per q per process).
+int certify_div4(rd_sim* s) {
+  static std::vector<std::pair<uint32_t, bool>> cache;
+  const float qf = (float)s->p.q;
+  uint32_t bits;
+  std::memcpy(&bits, &qf, 4);
+  for (const auto& c : cache)
+    if (c.first == bits) {
+      if (c.second) s->fast_mode = rdk::MODE_FOLD_DIV4;
+      return RD_OK;
+    }
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(s->d_scratch);
+  RD_CUDA(s, cudaMemsetAsync(d, 0, sizeof(unsigned long long), s->stream));
+  rdk::divcert_kernel<<<s->num_sms * 8, 256, 0, s->stream>>>(qf, d);
+  RD_CUDA(s, cudaGetLastError());
+  unsigned long long h = ~0ull;
+  RD_CUDA(s, cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  cache.push_back({bits, h == 0});
+  if (h == 0) s->fast_mode = rdk::MODE_FOLD_DIV4;
+  s->div4_mismatches = (int64_t)h;
+  return RD_OK;
+}
+
 char* plane_ptr(rd_sim* s, void* plane, int64_t b, int64_t local_row) {
   return (char*)plane +
          ((size_t)b * s->plane_stride + (size_t)(local_row + s->row_off) * s->pitch + (size_t)s->col_off) * s->esz;
@@ -590,6 +620,9 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
     if (s->num_sms < 1) s->num_sms = 148;
   }
   if (int rc = alloc_planes(s)) return fail(rc);
+  if (s->esz == 4 && s->fast_mode == rdk::MODE_FOLD && !(grid->flags & RD_REACTION_OFF)) {
+    if (int rc = certify_div4(s)) return fail(rc);
+  }
   // phi rows present in the host buffer: local [lo, hi)
   const int64_t lo = slab ? std::max<int64_t>(0, row0 - halo) - row0 : 0;
   const int64_t hi = slab ? std::min<int64_t>(Hg, row0 + s->H + halo) - row0 : s->H;
@@ -932,6 +965,7 @@ int rd_get_stats(rd_sim* s, rd_stats* out) {
   out->step_kernel_ms = s->acc_ms;
   out->timed_launches = s->acc_timed;
   out->tb_depth = s->K;
+  out->arith_mode = (s->g.flags & RD_NO_CHECKPOINT) ? rdk::MODE_PRECISE : s->fast_mode;
   return RD_OK;
 }
 

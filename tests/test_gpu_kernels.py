@@ -26,3 +26,28 @@ def test_fast_division_exhaustive(divcheck, q):
     r = json.loads(out.stdout)
     assert r["tested"] > 4_000_000_000
     assert r["mismatch_guarded"] == 0, r
+
+
+def test_certified_four_op_division_selected_for_table1_q():
+    """For Table-1 q the 4-op division is certified exhaustively at rd_create
+    and selected (arith_mode 3); a q where it is not exact keeps the 6-op
+    sequence (arith_mode 2); results are bitwise the oracle's either way."""
+    import numpy as np
+    import oracle
+    import paper_1901_06535_b200 as rd
+    from rdinputs import config
+    for q, mode in ((0.002, 3), (0.1, 2)):
+        p = rd.rd_params_default()
+        p.q = q
+        w = config(1, dtype=np.float32, steps=200)
+        sim = rd.Sim(w.phi_plane(0).astype(np.float32), dtype=np.float32, params=p)
+        assert sim.stats()["arith_mode"] == mode
+        for s, val, at in w.events[0]:
+            sim.stimulate(s, val, at)
+        sim.step(200)
+        u, v = sim.read(0)
+        sim.close()
+        u0, v0 = w.init_planes(0)
+        ref = oracle.run(u0, v0, w.phi_plane(0).astype(np.float32), 200, events=w.events[0],
+                         params=oracle.Params(q=q))
+        assert np.array_equal(u, ref.u) and np.array_equal(v, ref.v)
