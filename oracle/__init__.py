@@ -91,7 +91,8 @@ def lib():
             getattr(L, f"orc_run_{sfx}").restype = C.c_int
             getattr(L, f"orc_run_{sfx}").argtypes = [
                 i64, i64, P, P, P, C.POINTER(_Params), C.c_uint32, i64, i64,
-                C.POINTER(_Event), i64, C.POINTER(_Probe), i64, C.POINTER(C.c_int64), C.POINTER(_Fault)]
+                C.POINTER(_Event), i64, C.POINTER(_Probe), i64, C.POINTER(C.c_int64), C.POINTER(_Fault), i64, P]
+            getattr(L, f"orc_timelapse_record_{sfx}").argtypes = [i64, i64, P, P]
         L.orc_shape_contains.restype = C.c_int
         L.orc_shape_contains.argtypes = [C.POINTER(_Shape), i64, i64]
         L.orc_params_default.argtypes = [C.POINTER(_Params)]
@@ -195,14 +196,23 @@ class RunResult:
     first_fire: list = field(default_factory=list)
     status: int = 0
     fault: tuple | None = None
+    max_u: np.ndarray | None = None
+
+
+def timelapse_record(u: np.ndarray, max_u: np.ndarray) -> None:
+    """max_u := pointwise max(max_u, u), in place."""
+    getattr(lib(), f"orc_timelapse_record_{_sfx(u.dtype)}")(u.shape[0], u.shape[1], _ptr(np.ascontiguousarray(u)),
+                                                            _ptr(max_u))
 
 
 def run(u, v, phi, n_steps: int, events=(), probes=(), params: Params = Params(),
-        step0: int = 0, reaction_off: bool = False) -> RunResult:
+        step0: int = 0, reaction_off: bool = False, timelapse_stride: int = 0, max_u=None) -> RunResult:
     """Run one instance for n_steps.
 
     events: iterable of (shape_dict, value, at_step); probes: iterable of
-    (rect(y0,x0,y1,x1), threshold, stride). Returns copies of u, v.
+    (rect(y0,x0,y1,x1), threshold, stride). With timelapse_stride > 0 the
+    timelapse max_u (initial value max_u, default -inf) is recorded after every
+    step that is a multiple of it. Returns copies of u, v (and max_u).
     """
     u = np.array(u, copy=True, order="C")
     v = np.array(v, copy=True, order="C", dtype=u.dtype)
@@ -219,12 +229,16 @@ def run(u, v, phi, n_steps: int, events=(), probes=(), params: Params = Params()
         pr[k].stride = int(stride)
     ff = (C.c_int64 * max(1, len(probes)))(*([-1] * max(1, len(probes))))
     fault = _Fault(-1, -1, -1)
+    mu = None
+    if timelapse_stride > 0:
+        mu = (np.full(u.shape, -np.inf, dtype=u.dtype) if max_u is None
+              else np.array(max_u, dtype=u.dtype, copy=True, order="C"))
     st = getattr(lib(), f"orc_run_{_sfx(u.dtype)}")(
         u.shape[0], u.shape[1], _ptr(u), _ptr(v), _ptr(phi), C.byref(params.c()),
         ORC_REACTION_OFF if reaction_off else 0, step0, n_steps, ev, len(events), pr, len(probes), ff,
-        C.byref(fault))
+        C.byref(fault), int(timelapse_stride), _ptr(mu) if mu is not None else None)
     return RunResult(u, v, [ff[k] for k in range(len(probes))], st,
-                     (fault.step, fault.i, fault.j) if st != 0 else None)
+                     (fault.step, fault.i, fault.j) if st != 0 else None, mu)
 
 
 def run_batch(u, v, phi, n_steps: int, events_per=None, probes_per=None, params: Params = Params()):

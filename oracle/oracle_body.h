@@ -160,11 +160,20 @@ double FN(orc_probe_max)(int64_t H, int64_t W, const T* u, const orc_rect* r) {
  *     (u,v) <- step(u,v)                                         (a2-a5)
  *     if any non-finite cell: report first (row-major) cell, stop (a6)
  *     if (s+1) % stride == 0: latch probes with max u >= thr      (a6)
+ *     if (s+1) % tl_stride == 0: timelapse max_u := max(max_u, u) (f2)
  * u, v hold the state on return (at the failing step on error). */
+/* Timelapse record ("records a timelapse ... only the concentration
+ * of u is recorded over time"; SPEC.md:306-309 timelapse_record: max_u :=
+ * pointwise max(max_u, u)). A NaN u never replaces the recorded value. */
+void FN(orc_timelapse_record)(int64_t H, int64_t W, const T* u, T* max_u) {
+  for (int64_t k = 0; k < H * W; ++k)
+    if (u[k] > max_u[k]) max_u[k] = u[k];
+}
+
 int FN(orc_run)(int64_t H, int64_t W, T* u, T* v, const T* phi, const orc_params* p,
                 uint32_t flags, int64_t step0, int64_t n_steps, const orc_event* events,
                 int64_t n_events, const orc_probe* probes, int64_t n_probes,
-                int64_t* first_fire, orc_fault* fault) {
+                int64_t* first_fire, orc_fault* fault, int64_t tl_stride, T* tl_max) {
   T* u2 = (T*)malloc(sizeof(T) * (size_t)(H * W));
   T* v2 = (T*)malloc(sizeof(T) * (size_t)(H * W));
   if (!u2 || !v2) {
@@ -194,6 +203,7 @@ int FN(orc_run)(int64_t H, int64_t W, T* u, T* v, const T* phi, const orc_params
       status = ORC_ENONFINITE;
       break;
     }
+    if (tl_max && tl_stride > 0 && (s + 1) % tl_stride == 0) FN(orc_timelapse_record)(H, W, u, tl_max);
     for (int64_t pi = 0; pi < n_probes; ++pi) {
       const orc_probe* pr = &probes[pi];
       if (pr->stride > 0 && (s + 1) % pr->stride == 0 && first_fire[pi] < 0) {

@@ -93,7 +93,8 @@ void orc_set_num_threads(int n);
   int orc_run_##SFX(int64_t H, int64_t W, T* u, T* v, const T* phi, const orc_params* p,        \
                     uint32_t flags, int64_t step0, int64_t n_steps, const orc_event* events,     \
                     int64_t n_events, const orc_probe* probes, int64_t n_probes,                 \
-                    int64_t* first_fire, orc_fault* fault);
+                    int64_t* first_fire, orc_fault* fault, int64_t tl_stride, T* tl_max);        \
+  void orc_timelapse_record_##SFX(int64_t H, int64_t W, const T* u, T* max_u);
 ORC_DECL(double, f64)
 ORC_DECL(float, f32)
 #undef ORC_DECL

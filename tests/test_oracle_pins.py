@@ -416,3 +416,41 @@ def test_survey_cross_implementation_digest(sfx, dtype):
     r = oracle.run(u, v, w.phi_plane(0).astype(dtype), 1000, events=w.events[0])
     assert hashlib.sha256(r.u.astype("<" + r.u.dtype.str[1:]).tobytes()).hexdigest() == g["u_sha256"]
     assert hashlib.sha256(r.v.astype("<" + r.v.dtype.str[1:]).tobytes()).hexdigest() == g["v_sha256"]
+
+
+# ------------------------------------------------------ f2: timelapse max-u
+
+def test_timelapse_record_spec_examples():
+    """recording u=0.2 then u=0.5 gives 0.5; recording the same
+    state twice leaves the accumulator unchanged; NaN never replaces a value."""
+    m = np.full((2, 3), -np.inf)
+    oracle.timelapse_record(np.full((2, 3), 0.2), m)
+    oracle.timelapse_record(np.full((2, 3), 0.5), m)
+    assert np.all(m == 0.5)
+    oracle.timelapse_record(np.full((2, 3), 0.3), m)
+    assert np.all(m == 0.5)
+    x = np.full((2, 3), 0.7)
+    x[0, 1] = np.nan
+    oracle.timelapse_record(x, m)
+    assert m[0, 1] == 0.5 and m[1, 2] == 0.7
+
+
+def test_timelapse_run_equals_brute_force_max():
+    """The run's timelapse equals the pointwise max of u over the sampled
+    steps, computed from separately recorded snapshots, and a fresh
+    accumulator on a quiescent medium holds the rest state."""
+    w = config(1, dtype=np.float64, steps=300)
+    u, v = w.init_planes(0)
+    phi = w.phi_plane(0)
+    r = oracle.run(u, v, phi, 300, events=w.events[0], timelapse_stride=25)
+    snaps = []
+    uu, vv = u, v
+    for s in range(0, 300, 25):
+        rr = oracle.run(uu, vv, phi, 25, events=w.events[0], step0=s)
+        uu, vv = rr.u, rr.v
+        snaps.append(uu)
+    assert np.array_equal(r.max_u, np.max(np.stack(snaps), axis=0))
+    assert np.array_equal(r.u, uu)
+    z = np.zeros((6, 6))
+    q = oracle.run(z, z, np.full((6, 6), 0.054), 30000, timelapse_stride=30000)
+    assert np.allclose(q.max_u, _fixed_point(0.054), atol=1e-9)
