@@ -203,6 +203,21 @@ int rd_probe_latch(struct rd_sim* sim, int32_t b, const rd_rect* rect, double th
 /* First firing step of latched probe id, or -1 if it has not fired. Syncs. */
 int rd_probe_result(struct rd_sim* sim, int32_t id, int64_t* first_fire_step);
 
+/* ---- timelapse ---- */
+
+/* Record a timelapse of u ("records a timelapse of the
+ * reaction at a rate set by the user ... only the concentration of u is
+ * recorded over time"): after every step that is a positive multiple of
+ * stride, max_u := pointwise max(max_u, u) (a NaN u never
+ * replaces the recorded value). Fused into the stencil kernel's epilogue on
+ * sampled steps. stride > 0 enables and resets max_u to -inf; 0 disables.
+ * Errors: RD_EINVAL (stride < 0), RD_ENOMEM. */
+int rd_timelapse(struct rd_sim* sim, int32_t stride);
+
+/* Copy instance b's max_u to a HOST buffer [height][width] of dtype. Syncs.
+ * RD_ERANGE if no timelapse is enabled. */
+int rd_read_timelapse(struct rd_sim* sim, int32_t b, void* max_u_out);
+
 /* ---- row slabs for multi-GPU domain decomposition ---- */
 
 /* Create a handle owning rows [row0, row0 + grid->height) of a grid with

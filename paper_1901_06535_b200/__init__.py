@@ -21,7 +21,7 @@ from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_C
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
-           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_get_stats", "rd_set_profiling",
+           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -158,6 +158,14 @@ def rd_probe_result(h, pid: int) -> int:
     return out.value
 
 
+def rd_timelapse(h, stride: int) -> None:
+    _check(load().rd_timelapse(h, int(stride)), h)
+
+
+def rd_read_timelapse(h, b: int, out: np.ndarray) -> None:
+    _check(load().rd_read_timelapse(h, b, _ptr(out)), h)
+
+
 def rd_row_ptr(h, b: int, plane: int, row: int) -> tuple[int, int]:
     p, pitch = C.c_void_p(), C.c_int64()
     _check(load().rd_row_ptr(h, b, plane, row, C.byref(p), C.byref(pitch)), h)
@@ -242,6 +250,14 @@ class Sim:
 
     def probe_result(self, pid: int) -> int:
         return rd_probe_result(self.h, pid)
+
+    def timelapse(self, stride: int) -> None:
+        rd_timelapse(self.h, stride)
+
+    def read_timelapse(self, b: int = 0) -> np.ndarray:
+        out = np.empty((self.H, self.W), dtype=self.dtype)
+        rd_read_timelapse(self.h, b, out)
+        return out
 
     def fault(self):
         return rd_get_fault(self.h)

@@ -58,6 +58,9 @@ struct rd_sim {
   void* phi = nullptr;
   void* ck_u = nullptr;
   void* ck_v = nullptr;
+  void* tl = nullptr;     // f2: timelapse max_u planes
+  void* ck_tl = nullptr;
+  int32_t tl_stride = 0;
   int cur = 0;
   int64_t step = 0;
   int32_t ghost_valid = 0;  // slab: ghost rows still valid in the current buffers
@@ -246,6 +249,7 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_
   a.k = make_consts<T>(s->p);
   a.fault_key = s->d_fault;
   a.precise_flag = s->d_precise;
+  a.tl = (s->tl_stride > 0 && (s->step + K) % s->tl_stride == 0) ? origin<T>(s, s->tl) : nullptr;
   const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
   const int64_t grid = std::min<int64_t>(tasks, ctas);
   rdk::tb_kernel<T, K, V, REACT, MODE><<<(unsigned)grid, 32, 0, s->stream>>>(a);
@@ -450,6 +454,7 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
       if (ev.at > s->step) next = std::min(next, ev.at);
     for (const auto& q : s->probes)
       if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
+    if (s->tl_stride > 0) next = std::min(next, (s->step / s->tl_stride + 1) * (int64_t)s->tl_stride);
     while (s->step < next) {
       const int k = (int)std::min<int64_t>(kmax, next - s->step);
       if ((rc = launch_tb(s, k))) return rc;
@@ -721,8 +726,9 @@ int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi
 int rd_destroy(rd_sim* s) {
   if (!s) return RD_OK;
   if (s->stream) cudaStreamSynchronize(s->stream);
-  void* ps[] = {s->u[0], s->u[1], s->v[0], s->v[1], s->phi, s->ck_u, s->ck_v, s->d_probes, s->d_first, s->d_first_ck,
-                s->d_fault, s->d_flag, s->d_scratch};
+  void* ps[] = {s->u[0],  s->u[1],       s->v[0],  s->v[1],   s->phi,       s->ck_u,     s->ck_v,
+                s->tl,    s->ck_tl,      s->d_probes, s->d_first, s->d_first_ck, s->d_fault, s->d_flag,
+                s->d_scratch};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& e : s->ev_pool) {
@@ -814,6 +820,7 @@ int rd_step(rd_sim* s, int64_t n) {
     if (!s->probes.empty())
       RD_CUDA(s, cudaMemcpyAsync(s->d_first_ck, s->d_first, sizeof(long long) * s->probes.size(),
                                  cudaMemcpyDeviceToDevice, s->stream));
+    if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->ck_tl, s->tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
     events0 = s->events;
   }
   if ((rc = run_range(s, step0 + n, s->K))) return rc;
@@ -834,6 +841,7 @@ int rd_step(rd_sim* s, int64_t n) {
     if (!s->probes.empty())
       RD_CUDA(s, cudaMemcpyAsync(s->d_first, s->d_first_ck, sizeof(long long) * s->probes.size(),
                                  cudaMemcpyDeviceToDevice, s->stream));
+    if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->tl, s->ck_tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
     s->events = events0;
     s->step = step0;
     s->ghost_valid = (int32_t)s->halo;
@@ -928,6 +936,36 @@ int rd_probe_result(rd_sim* s, int32_t id, int64_t* first) {
   RD_CUDA(s, cudaMemcpyAsync(&h, s->d_first + id, sizeof h, cudaMemcpyDeviceToHost, s->stream));
   RD_CUDA(s, cudaStreamSynchronize(s->stream));
   *first = h;
+  return RD_OK;
+}
+
+int rd_timelapse(rd_sim* s, int32_t stride) {
+  if (!s) return RD_EINVAL;
+  if (stride < 0) return set_err(s, RD_EINVAL, "stride must be >= 0");
+  s->tl_stride = stride;
+  if (stride == 0) return RD_OK;
+  const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
+  if (!s->tl) {
+    RD_CUDA(s, cudaMalloc(&s->tl, bytes));
+    if (!(s->g.flags & RD_NO_CHECKPOINT)) RD_CUDA(s, cudaMalloc(&s->ck_tl, bytes));
+  }
+  const int64_t n = (int64_t)s->B * s->plane_stride;
+  if (s->esz == 4)
+    rdk::fill_kernel<float><<<s->num_sms * 4, 256, 0, s->stream>>>((float*)s->tl, n, -INFINITY);
+  else
+    rdk::fill_kernel<double><<<s->num_sms * 4, 256, 0, s->stream>>>((double*)s->tl, n, -INFINITY);
+  RD_CUDA(s, cudaGetLastError());
+  s->st.launches++;
+  return RD_OK;
+}
+
+int rd_read_timelapse(rd_sim* s, int32_t b, void* out) {
+  if (!s || !out) return RD_EINVAL;
+  if (int rc = check_b(s, b)) return rc;
+  if (!s->tl) return set_err(s, RD_ERANGE, "no timelapse enabled (rd_timelapse)");
+  RD_CUDA(s, cudaMemcpy2DAsync(out, s->W * s->esz, plane_ptr(s, s->tl, b, 0), s->pitch * s->esz, s->W * s->esz, s->H,
+                               cudaMemcpyDeviceToHost, s->stream));
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
   return RD_OK;
 }
 

@@ -234,3 +234,25 @@ def test_fast_division_guard_replay(tb):
     assert_bitwise(u, ref.u, "u")
     assert_bitwise(v, ref.v, "v")
     sim.close()
+
+
+@pytest.mark.parametrize("dtype", DT, ids=IDS)
+@pytest.mark.parametrize("stride,tb", [(25, 4), (7, 4), (50, 1), (3, 8)])
+def test_timelapse_matches_oracle(dtype, stride, tb):
+    """f2: the fused timelapse max_u, recorded after
+    every multiple of stride, equals the oracle's bitwise; splitting rd_step
+    calls does not change it."""
+    w = _noise_workload(60, 90, dtype, 140)
+    u0, v0 = w.init_planes(0)
+    ref = oracle.run(u0, v0, w.phi_plane(0).astype(dtype), 140, events=w.events[0], timelapse_stride=stride)
+    for splits in ([140], [13, 50, 77]):
+        sim = rd.Sim(w.phi_plane(0).astype(dtype), dtype=dtype, tb_depth=tb)
+        sim.write(0, u0, v0)
+        for s, val, at in w.events[0]:
+            sim.stimulate(s, val, at)
+        sim.timelapse(stride)
+        for n in splits:
+            sim.step(n)
+        assert_bitwise(sim.read_timelapse(0), ref.max_u, f"max_u splits={splits}")
+        assert_bitwise(sim.read(0)[0], ref.u, "u")
+        sim.close()
