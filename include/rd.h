@@ -203,6 +203,16 @@ int rd_probe_latch(struct rd_sim* sim, int32_t b, const rd_rect* rect, double th
 /* First firing step of latched probe id, or -1 if it has not fired. Syncs. */
 int rd_probe_result(struct rd_sim* sim, int32_t id, int64_t* first_fire_step);
 
+/* ---- per-instance parameters (batched sweeps) ---- */
+
+/* Set the Eq. 1 parameters (Table 1) of
+ * instance b, or of every instance (b = -1, which also drops per-instance
+ * sets). Lets one batched launch sweep eps, f, q, Du, dt, dx across
+ * instances (e.g. a calibration bisection); phi is already per instance.
+ * Validation as rd_create (RD_EPARAM); per-instance sets need batch <= 32
+ * (RD_EINVAL). Takes effect from the next rd_step. */
+int rd_set_params(struct rd_sim* sim, int32_t b, const rd_params* params);
+
 /* ---- timelapse ---- */
 
 /* Record a timelapse of u ("records a timelapse of the

@@ -47,6 +47,7 @@ struct rd_sim {
   int64_t row_off = 0;  // margin + guard rows: row offset of local row 0
   int64_t col_off = 0;  // mirrored ghost columns left of column 0
   int32_t margin = 0;   // ghost rows above/below (slab halo or mirror margin)
+  std::vector<rd_params> pinst;  // f1: per-instance parameters (empty = all use p)
   int64_t div4_mismatches = -1;  // result of the 4-op division certification (-1: not run)
   int fast_mode = 0;    // rdk::MODE_FOLD[_DIV4] when 1/dx^2 is a power of two, else MODE_PRECISE
   int64_t grow0 = 0, Hg = 0;
@@ -246,7 +247,13 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_
   a.pad_ = 0;
   a.grow0 = s->grow0;
   a.H_global = s->Hg;
-  a.k = make_consts<T>(s->p);
+  a.per_instance = s->pinst.empty() ? 0 : 1;
+  a.pad2_ = 0;
+  if (s->pinst.empty()) {
+    a.k[0] = make_consts<T>(s->p);
+  } else {
+    for (int64_t b = 0; b < s->B; ++b) a.k[b] = make_consts<T>(s->pinst[b]);
+  }
   a.fault_key = s->d_fault;
   a.precise_flag = s->d_precise;
   a.tl = (s->tl_stride > 0 && (s->step + K) % s->tl_stride == 0) ? origin<T>(s, s->tl) : nullptr;
@@ -520,14 +527,14 @@ int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
 // Enables the 4-op fp32 division if, for this handle's q, it equals IEEE
 // div.rn on every input the reaction can produce (exhaustive check of all
 // 2^32 fp32 values of C on the GPU, a few ms; cached per q per process).
-int certify_div4(rd_sim* s) {
+int certify_q(rd_sim* s, double q, bool* ok) {
   static std::vector<std::pair<uint32_t, bool>> cache;
-  const float qf = (float)s->p.q;
+  const float qf = (float)q;
   uint32_t bits;
   std::memcpy(&bits, &qf, 4);
   for (const auto& c : cache)
     if (c.first == bits) {
-      if (c.second) s->fast_mode = rdk::MODE_FOLD_DIV4;
+      *ok = c.second;
       return RD_OK;
     }
   unsigned long long* d = reinterpret_cast<unsigned long long*>(s->d_scratch);
@@ -538,8 +545,35 @@ int certify_div4(rd_sim* s) {
   RD_CUDA(s, cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s->stream));
   RD_CUDA(s, cudaStreamSynchronize(s->stream));
   cache.push_back({bits, h == 0});
-  if (h == 0) s->fast_mode = rdk::MODE_FOLD_DIV4;
   s->div4_mismatches = (int64_t)h;
+  *ok = h == 0;
+  return RD_OK;
+}
+
+// Whether 1/dx^2 is a power of two, so Du may be folded into it exactly.
+bool foldable(const rd_params& p) {
+  const double inv = 1.0 / (p.dx * p.dx);
+  int ex = 0;
+  return std::frexp(inv, &ex) == 0.5 && ex > -100 && ex < 100;
+}
+
+// Arithmetic mode for the handle's parameter set(s): FOLD when every 1/dx^2
+// is a power of two, FOLD_DIV4 when additionally (fp32, reaction on) the
+// 4-op division is certified for every q; else PRECISE.
+int choose_mode(rd_sim* s) {
+  std::vector<rd_params> sets = s->pinst.empty() ? std::vector<rd_params>{s->p} : s->pinst;
+  bool fold = true;
+  for (const auto& p : sets) fold = fold && foldable(p);
+  s->fast_mode = fold ? rdk::MODE_FOLD : rdk::MODE_PRECISE;
+  if (fold && s->esz == 4 && !(s->g.flags & RD_REACTION_OFF)) {
+    bool all = true;
+    for (const auto& p : sets) {
+      bool ok = false;
+      if (int rc = certify_q(s, p.q, &ok)) return rc;
+      all = all && ok;
+    }
+    if (all) s->fast_mode = rdk::MODE_FOLD_DIV4;
+  }
   return RD_OK;
 }
 
@@ -594,14 +628,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   s->col_off = rdk::kMarginCols;
   s->rows_alloc = s->H + 2 * s->row_off;
   s->plane_stride = s->rows_alloc * s->pitch;
-  {
-    // Du may be folded into the Laplacian scale when 1/dx^2 is a power of two
-    // in the working precision (then du*(d*inv_dx2) == d*(du*inv_dx2) exactly)
-    const double inv = 1.0 / (params->dx * params->dx);
-    int ex = 0;
-    const double fr = std::frexp(inv, &ex);
-    s->fast_mode = (fr == 0.5 && ex > -100 && ex < 100) ? rdk::MODE_FOLD : rdk::MODE_PRECISE;
-  }
+
   s->ghost_valid = (int32_t)s->halo;
   s->K = grid->tb_depth > 0 ? grid->tb_depth : auto_tb(s);
   if (slab && s->K > s->halo) s->K = (int)s->halo;
@@ -625,9 +652,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
     if (s->num_sms < 1) s->num_sms = 148;
   }
   if (int rc = alloc_planes(s)) return fail(rc);
-  if (s->esz == 4 && s->fast_mode == rdk::MODE_FOLD && !(grid->flags & RD_REACTION_OFF)) {
-    if (int rc = certify_div4(s)) return fail(rc);
-  }
+  if (int rc = choose_mode(s)) return fail(rc);
   // phi rows present in the host buffer: local [lo, hi)
   const int64_t lo = slab ? std::max<int64_t>(0, row0 - halo) - row0 : 0;
   const int64_t hi = slab ? std::min<int64_t>(Hg, row0 + s->H + halo) - row0 : s->H;
@@ -937,6 +962,23 @@ int rd_probe_result(rd_sim* s, int32_t id, int64_t* first) {
   RD_CUDA(s, cudaStreamSynchronize(s->stream));
   *first = h;
   return RD_OK;
+}
+
+int rd_set_params(rd_sim* s, int32_t b, const rd_params* p) {
+  if (!s || !p) return RD_EINVAL;
+  if (b < -1 || b >= s->B) return set_err(s, RD_ERANGE, "instance %d out of range", b);
+  std::string why;
+  if (int rc = check_params(p, &why)) return set_err(s, rc, "%s", why.c_str());
+  if (b == -1) {
+    s->p = *p;
+    s->pinst.clear();
+  } else {
+    if (s->B > rdk::kMaxParamSets)
+      return set_err(s, RD_EINVAL, "per-instance parameters need batch <= %d", rdk::kMaxParamSets);
+    if (s->pinst.empty()) s->pinst.assign((size_t)s->B, s->p);
+    s->pinst[(size_t)b] = *p;
+  }
+  return choose_mode(s);
 }
 
 int rd_timelapse(rd_sim* s, int32_t stride) {
