@@ -93,6 +93,9 @@ def lib():
                 i64, i64, P, P, P, C.POINTER(_Params), C.c_uint32, i64, i64,
                 C.POINTER(_Event), i64, C.POINTER(_Probe), i64, C.POINTER(C.c_int64), C.POINTER(_Fault), i64, P]
             getattr(L, f"orc_timelapse_record_{sfx}").argtypes = [i64, i64, P, P]
+            getattr(L, f"orc_rest_fill_{sfx}").argtypes = [i64, i64, P, P, P, C.POINTER(_Params)]
+        L.orc_rest_state.restype = C.c_double
+        L.orc_rest_state.argtypes = [C.c_double, C.POINTER(_Params)]
         L.orc_shape_contains.restype = C.c_int
         L.orc_shape_contains.argtypes = [C.POINTER(_Shape), i64, i64]
         L.orc_params_default.argtypes = [C.POINTER(_Params)]
@@ -197,6 +200,21 @@ class RunResult:
     status: int = 0
     fault: tuple | None = None
     max_u: np.ndarray | None = None
+
+
+def rest_state(phi: float, params: Params = Params()) -> float:
+    """u* = v* of the homogeneous medium with excitability phi, by fp64
+    bisection (SPEC.md:85-93)."""
+    return lib().orc_rest_state(float(phi), C.byref(params.c()))
+
+
+def rest_fill(phi: np.ndarray, params: Params = Params()):
+    """Quiescent initial planes u = v = u*(phi) per cell."""
+    phi = np.ascontiguousarray(phi)
+    u, v = np.empty_like(phi), np.empty_like(phi)
+    getattr(lib(), f"orc_rest_fill_{_sfx(phi.dtype)}")(phi.shape[0], phi.shape[1], _ptr(phi), _ptr(u), _ptr(v),
+                                                        C.byref(params.c()))
+    return u, v
 
 
 def timelapse_record(u: np.ndarray, max_u: np.ndarray) -> None:

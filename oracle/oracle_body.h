@@ -162,6 +162,17 @@ double FN(orc_probe_max)(int64_t H, int64_t W, const T* u, const orc_rect* r) {
  *     if (s+1) % stride == 0: latch probes with max u >= thr      (a6)
  *     if (s+1) % tl_stride == 0: timelapse max_u := max(max_u, u) (f2)
  * u, v hold the state on return (at the failing step on error). */
+/* Quiescent initial state: u = v = u*(phi) of
+ * each cell, computed in fp64 from the cell's phi (as stored in T) and rounded
+ * once to T. */
+void FN(orc_rest_fill)(int64_t H, int64_t W, const T* phi, T* u, T* v, const orc_params* p) {
+  for (int64_t k = 0; k < H * W; ++k) {
+    T us = (T)orc_rest_state((double)phi[k], p);
+    u[k] = us;
+    v[k] = us;
+  }
+}
+
 /* Timelapse record ("records a timelapse ... only the concentration
  * of u is recorded over time"; SPEC.md:306-309 timelapse_record: max_u :=
  * pointwise max(max_u, u)). A NaN u never replaces the recorded value. */

@@ -59,6 +59,33 @@ int orc_shape_contains(const orc_shape* s, int64_t i, int64_t j) {
   return 0;
 }
 
+/* Homogeneous rest state (SPEC.md:85-93 steady_state: "v* = u* ... found by
+ * bisection on u in (0, 1); the smallest positive root"). With v = u the
+ * reaction of Eq. 1 vanishes where
+ *   F(u) = (u - u*u) - ((f*u + phi) * ((u - q)/(u + q))) = 0,
+ * F(0+) = phi > 0 and F(1) < 0, and the cubic it reduces to has exactly one
+ * positive root. Bisection in fp64 until the midpoint no longer splits the
+ * interval; returns lo (F(lo) > 0 >= F(hi), hi = next double after lo). */
+double orc_rest_state(double phi, const orc_params* p) {
+  const double f = p->f, q = p->q;
+  double lo = 0.0, hi = 1.0;
+  for (;;) {
+    double mid = (lo + hi) * 0.5;
+    if (!(mid > lo && mid < hi)) break;
+    double r = (mid - q) / (mid + q);
+    double w = f * mid;
+    w = w + phi;
+    double uu = mid * mid;
+    double F = mid - uu;
+    F = F - (w * r);
+    if (F > 0.0)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
 #define T double
 #define SFX f64
 #include "oracle_body.h"

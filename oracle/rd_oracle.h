@@ -77,6 +77,7 @@ typedef struct {
 } orc_fault;
 
 void orc_params_default(orc_params* p);
+double orc_rest_state(double phi, const orc_params* p);
 int orc_shape_contains(const orc_shape* s, int64_t i, int64_t j);
 int orc_num_threads(void);
 void orc_set_num_threads(int n);
@@ -94,7 +95,8 @@ void orc_set_num_threads(int n);
                     uint32_t flags, int64_t step0, int64_t n_steps, const orc_event* events,     \
                     int64_t n_events, const orc_probe* probes, int64_t n_probes,                 \
                     int64_t* first_fire, orc_fault* fault, int64_t tl_stride, T* tl_max);        \
-  void orc_timelapse_record_##SFX(int64_t H, int64_t W, const T* u, T* max_u);
+  void orc_timelapse_record_##SFX(int64_t H, int64_t W, const T* u, T* max_u);                   \
+  void orc_rest_fill_##SFX(int64_t H, int64_t W, const T* phi, T* u, T* v, const orc_params* p);
 ORC_DECL(double, f64)
 ORC_DECL(float, f32)
 #undef ORC_DECL

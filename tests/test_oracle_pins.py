@@ -454,3 +454,30 @@ def test_timelapse_run_equals_brute_force_max():
     z = np.zeros((6, 6))
     q = oracle.run(z, z, np.full((6, 6), 0.054), 30000, timelapse_stride=30000)
     assert np.allclose(q.max_u, _fixed_point(0.054), atol=1e-9)
+
+
+# ------------------------------------------------------- f4: rest-state init
+
+@pytest.mark.parametrize("phi", [0.054, 0.0975, 0.119, 0.2])
+def test_rest_state_bisection_is_the_cubic_root(phi):
+    """the bisection's u* is the closed-form cubic root
+    (numpy.roots) to ~1 ulp, its reaction residual vanishes, and it is
+    invariant under scaling eps."""
+    us = oracle.rest_state(phi)
+    assert us == pytest.approx(_fixed_point(phi), rel=1e-13, abs=0)
+    du, _ = oracle.reaction(us, us, phi)
+    assert abs(du) < 1e-10
+    assert oracle.rest_state(phi, oracle.Params(eps=2 * 0.0243)) == us
+
+
+def test_rest_fill_is_stationary():
+    """A quiescent medium filled with u*(phi) per cell stays at rest: uniform
+    regions stay bitwise uniform and nothing fires over 2000 steps."""
+    phi = np.full((30, 40), 0.054)
+    phi[10:20, :] = 0.0975
+    u, v = oracle.rest_fill(phi)
+    assert np.all(u == v) and u[0, 0] == oracle.rest_state(0.054) and u[15, 0] == oracle.rest_state(0.0975)
+    r = oracle.run(u, v, phi, 2000, probes=[((0, 0, 30, 40), 0.1, 50)])
+    assert r.first_fire == [-1] and np.abs(r.u - u).max() < 1e-4
+    u32, _ = oracle.rest_fill(phi.astype(np.float32))
+    assert u32.dtype == np.float32 and u32[0, 0] == np.float32(oracle.rest_state(float(np.float32(0.054))))
