@@ -213,6 +213,15 @@ int rd_probe_result(struct rd_sim* sim, int32_t id, int64_t* first_fire_step);
  * (RD_EINVAL). Takes effect from the next rd_step. */
 int rd_set_params(struct rd_sim* sim, int32_t b, const rd_params* params);
 
+/* ---- quiescent initial state ---- */
+
+/* Set u = v = u*(phi) in every cell of instance b (-1 = all): the homogeneous
+ * rest state of Eq. 1 for the cell's own phi, i.e. the root of
+ * (u - u^2) - (f u + phi)(u - q)/(u + q) = 0 (PAPER.md:91 with v = u), found by
+ * fp64 bisection on (0, 1) and rounded once to the dtype (SPEC.md:85-93,
+ * :107: "quiescent medium = homogeneous (u*, v*) from steady_state"). */
+int rd_init_rest(struct rd_sim* sim, int32_t b);
+
 /* ---- timelapse ---- */
 
 /* Record a timelapse of u ("records a timelapse of the

@@ -21,7 +21,7 @@ from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_C
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
-           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_set_params", "rd_get_stats", "rd_set_profiling",
+           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_set_params", "rd_init_rest", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -162,6 +162,10 @@ def rd_set_params(h, b: int, params: _lib.rd_params) -> None:
     _check(load().rd_set_params(h, int(b), C.byref(params)), h)
 
 
+def rd_init_rest(h, b: int = -1) -> None:
+    _check(load().rd_init_rest(h, int(b)), h)
+
+
 def rd_timelapse(h, stride: int) -> None:
     _check(load().rd_timelapse(h, int(stride)), h)
 
@@ -258,6 +262,10 @@ class Sim:
     def set_params(self, b: int, params) -> None:
         """Per-instance Eq. 1 parameters (b = -1: all instances)."""
         rd_set_params(self.h, b, params)
+
+    def init_rest(self, b: int = -1) -> None:
+        """Quiescent start: u = v = u*(phi) per cell."""
+        rd_init_rest(self.h, b)
 
     def timelapse(self, stride: int) -> None:
         rd_timelapse(self.h, stride)

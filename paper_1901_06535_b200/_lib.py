@@ -72,6 +72,7 @@ SYMBOLS = [
     ("rd_probe_latch", C.c_int, [P, i32, C.POINTER(rd_rect), dbl, i32, C.POINTER(C.c_int32)]),
     ("rd_probe_result", C.c_int, [P, i32, C.POINTER(C.c_int64)]),
     ("rd_set_params", C.c_int, [P, i32, C.POINTER(rd_params)]),
+    ("rd_init_rest", C.c_int, [P, i32]),
     ("rd_timelapse", C.c_int, [P, i32]),
     ("rd_read_timelapse", C.c_int, [P, i32, P]),
     ("rd_row_ptr", C.c_int, [P, i32, i32, i64, C.POINTER(P), C.POINTER(C.c_int64)]),

@@ -981,6 +981,27 @@ int rd_set_params(rd_sim* s, int32_t b, const rd_params* p) {
   return choose_mode(s);
 }
 
+int rd_init_rest(rd_sim* s, int32_t b) {
+  if (!s) return RD_EINVAL;
+  if (b < -1 || b >= s->B) return set_err(s, RD_ERANGE, "instance %d out of range", b);
+  const int32_t b0 = b < 0 ? 0 : b, nb = b < 0 ? (int32_t)s->B : 1;
+  for (int32_t i = b0; i < b0 + nb; ++i) {
+    const rd_params& p = s->pinst.empty() ? s->p : s->pinst[(size_t)i];
+    dim3 grid((unsigned)std::min<int64_t>(((s->r_hi - s->r_lo) * s->W + 255) / 256, s->num_sms * 8), 1);
+    if (s->esz == 4)
+      rdk::rest_fill_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, s->phi), origin<float>(s, s->u[s->cur]),
+                                                                origin<float>(s, s->v[s->cur]), s->plane_stride,
+                                                                s->pitch, s->r_lo, s->r_hi, (int32_t)s->W, p.f, p.q, i);
+    else
+      rdk::rest_fill_kernel<double><<<grid, 256, 0, s->stream>>>(
+          origin<double>(s, s->phi), origin<double>(s, s->u[s->cur]), origin<double>(s, s->v[s->cur]),
+          s->plane_stride, s->pitch, s->r_lo, s->r_hi, (int32_t)s->W, p.f, p.q, i);
+    RD_CUDA(s, cudaGetLastError());
+    s->st.launches++;
+  }
+  return launch_mirror(s, s->u[s->cur], s->v[s->cur], nullptr, s->r_lo, s->r_hi);
+}
+
 int rd_timelapse(rd_sim* s, int32_t stride) {
   if (!s) return RD_EINVAL;
   if (stride < 0) return set_err(s, RD_EINVAL, "stride must be >= 0");

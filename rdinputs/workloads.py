@@ -33,6 +33,7 @@ class Workload:
     init: Callable | None = None   # init(b, row0, rows) -> (u, v) in dtype, or None for zeros
     expect: dict = field(default_factory=dict)   # the paper's outcome for each instance
     meta: dict = field(default_factory=dict)
+    rest_init: bool = False        # start from the quiescent rest state u=v=u*(phi) (computed by each side)
 
     def phi_plane(self, b: int, row0: int = 0, rows: int | None = None) -> np.ndarray:
         rows = self.H if rows is None else rows
@@ -114,6 +115,21 @@ def _cfg5(dtype=np.float32, steps=2000, H=65536, W=65536, n_obstacles=256, **kw)
                     meta={"obstacles": rects})
 
 
+def spiral_seed(dtype=np.float64, steps=40000, H=160, W=160, delay=3500, offset=22, radius=5,
+                staggered=True) -> Workload:
+    """f4: "starting a simple target wave, then starting another
+    wave inside the target wave shortly afterwards ... slightly to one side
+    of the centre" on a quiescent medium. With the second stimulus
+    `offset` cells right of the centre at step `delay`, the broken wave
+    re-enters and activity is sustained; a single target wave (staggered=False)
+    leaves the domain."""
+    phi = np.full((H, W), 0.054)
+    ev = [({"kind": "disc", "cy2": H - 1, "cx2": W - 1, "r": radius}, 1.0, 0)]
+    if staggered:
+        ev.append(({"kind": "disc", "cy2": H - 1, "cx2": W - 1 + 2 * offset, "r": radius}, 1.0, delay))
+    return Workload("f4_spiral" if staggered else "f4_target", H, W, 1, dtype, steps, [phi], [ev], rest_init=True)
+
+
 _CFGS = {1: _cfg1, 2: _cfg2, 3: _cfg3, 4: _cfg4, 5: _cfg5}
 
 
@@ -123,4 +139,4 @@ def config(n: int, **kw) -> Workload:
     return _CFGS[n](**kw)
 
 
-__all__ = ["Workload", "config", "phi_from_rects"]
+__all__ = ["Workload", "config", "phi_from_rects", "spiral_seed"]

@@ -83,3 +83,18 @@ def test_diode_directionality(diode_runs):
     for r in runs:
         for (umin, umax, vmin, vmax) in r[3]:
             assert -0.1 < umin and umax < 1.1 and -0.01 < vmin and vmax < 1.1
+
+
+def test_staggered_stimuli_sustain_activity():
+    """f4 / PAPER.md:343-347: on a quiescent medium a second stimulus
+    placed beside the first target wave after a delay breaks it into a
+    re-entrant (spiral) wave: activity is sustained at step 40000, while a
+    single target wave has left the domain by step 12000."""
+    from rdinputs import spiral_seed
+    w = spiral_seed()
+    u, v = oracle.rest_fill(w.phi_plane(0))
+    r = oracle.run(u, v, w.phi_plane(0), w.steps, events=w.events[0])
+    assert (r.u > 0.1).mean() > 0.05
+    c = spiral_seed(staggered=False, steps=12000)
+    r1 = oracle.run(u, v, c.phi_plane(0), c.steps, events=c.events[0])
+    assert r1.u.max() < 0.01

@@ -256,3 +256,34 @@ def test_timelapse_matches_oracle(dtype, stride, tb):
         assert_bitwise(sim.read_timelapse(0), ref.max_u, f"max_u splits={splits}")
         assert_bitwise(sim.read(0)[0], ref.u, "u")
         sim.close()
+
+
+@pytest.mark.parametrize("dtype", DT, ids=IDS)
+def test_rest_init_and_spiral_seeding(dtype):
+    """f4: rd_init_rest gives the oracle's quiescent planes bitwise (per-cell
+    u*(phi) on a two-level phi map), and the staggered spiral-seeding run
+     equals the oracle bitwise at step 40000 with sustained
+    activity."""
+    from rdinputs import spiral_seed
+    phi = np.full((50, 70), 0.054)
+    phi[20:30, 10:60] = 0.119
+    sim = rd.Sim(phi.astype(dtype), dtype=dtype)
+    sim.init_rest()
+    u, v = sim.read(0)
+    ru, rv = oracle.rest_fill(phi.astype(dtype))
+    assert_bitwise(u, ru, "u*")
+    assert_bitwise(v, rv, "v*")
+    sim.close()
+    w = spiral_seed(dtype=dtype)
+    sim = rd.Sim(w.phi_plane(0).astype(dtype), dtype=dtype)
+    sim.init_rest()
+    for s, val, at in w.events[0]:
+        sim.stimulate(s, val, at)
+    sim.step(w.steps)
+    u, v = sim.read(0)
+    sim.close()
+    u0, v0 = oracle.rest_fill(w.phi_plane(0).astype(dtype))
+    ref = oracle.run(u0, v0, w.phi_plane(0).astype(dtype), w.steps, events=w.events[0])
+    assert_bitwise(u, ref.u, "u")
+    assert_bitwise(v, ref.v, "v")
+    assert (u > 0.1).mean() > 0.05
