@@ -142,7 +142,8 @@ typedef struct {
 void rd_params_default(rd_params* p);
 
 /* Create a handle. phi_map: HOST buffer [batch][height][width] of the grid's
- * dtype (copied; must be finite). u = v = 0 initially (R-10).
+ * dtype (copied; must be finite), or NULL for phi = 0 everywhere (then paint
+ * it with rd_paint_phi). u = v = 0 initially (R-10).
  * Errors: RD_EINVAL, RD_EPARAM, RD_ENONFINITE (phi), RD_ENOMEM, RD_ECUDA. */
 int rd_create(const rd_grid* grid, const rd_params* params, const void* phi_map, struct rd_sim** out);
 
@@ -212,6 +213,23 @@ int rd_probe_result(struct rd_sim* sim, int32_t id, int64_t* first_fire_step);
  * Validation as rd_create (RD_EPARAM); per-instance sets need batch <= 32
  * (RD_EINVAL). Takes effect from the next rd_step. */
 int rd_set_params(struct rd_sim* sim, int32_t b, const rd_params* params);
+
+/* ---- seeded initial state on the device (config 4/5 inputs) ---- */
+
+/* phi := value on the rectangle (global rows/columns, clipped; NULL = the
+ * whole grid) of instance b (-1 = all): the per-pixel excitability map of
+ * PAPER.md:108-110 built on the device (e.g. a background plus obstacle
+ * rectangles, BASELINE.json configs[4]) instead of uploaded. */
+int rd_paint_phi(struct rd_sim* sim, int32_t b, const rd_rect* rect, double value);
+
+/* Fill u (planes bit 1) and/or v (bit 2) of instance b (-1 = all) with the
+ * counter-based noise of DESIGN.md §4 in GLOBAL coordinates (so slabs of any
+ * decomposition get the same values, ghost rows included): value at global
+ * cell (i, j) of plane p = ((R(seed, p<<62 | i*W + j) >> 40) * 2^-24) *
+ * amplitude, R(s, n) = SM(SM(s) + n), SM = SplitMix64; fp64 then rounded once
+ * (BASELINE.json configs[3]: "u,v initialised i.i.d. uniform[0,0.1] from
+ * seed"). Input generation only; equals rdinputs.noise_plane bitwise. */
+int rd_fill_noise(struct rd_sim* sim, int32_t b, uint32_t planes, uint64_t seed, double amplitude);
 
 /* ---- quiescent initial state ---- */
 

@@ -21,7 +21,7 @@ from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_C
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
-           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_set_params", "rd_init_rest", "rd_get_stats", "rd_set_profiling",
+           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -68,12 +68,13 @@ def rd_params_default() -> _lib.rd_params:
     return p
 
 
-def rd_create(width: int, height: int, phi_map: np.ndarray, *, batch: int = 1, dtype=np.float32,
+def rd_create(width: int, height: int, phi_map: np.ndarray | None, *, batch: int = 1, dtype=np.float32,
               tb_depth: int = 0, flags: int = 0, params: _lib.rd_params | None = None, pitch: int = 0):
-    """rd_create(grid, params, phi_map): phi_map is [batch][height][width] on the host."""
+    """rd_create(grid, params, phi_map): phi_map is [batch][height][width] on
+    the host, or None for phi = 0 (paint it with rd_paint_phi)."""
     dt = np.dtype(dtype)
-    phi = np.ascontiguousarray(phi_map, dtype=dt)
-    assert phi.size == batch * height * width
+    phi = None if phi_map is None else np.ascontiguousarray(phi_map, dtype=dt)
+    assert phi is None or phi.size == batch * height * width
     g = _lib.rd_grid(width, height, batch, _DT[dt], tb_depth, flags, pitch)
     p = params or rd_params_default()
     h = C.c_void_p()
@@ -84,7 +85,7 @@ def rd_create(width: int, height: int, phi_map: np.ndarray, *, batch: int = 1, d
 def rd_create_slab(width: int, height: int, phi_slab: np.ndarray, row0: int, height_global: int, halo: int, *,
                    batch: int = 1, dtype=np.float32, tb_depth: int = 0, flags: int = 0, params=None):
     dt = np.dtype(dtype)
-    phi = np.ascontiguousarray(phi_slab, dtype=dt)
+    phi = None if phi_slab is None else np.ascontiguousarray(phi_slab, dtype=dt)
     g = _lib.rd_grid(width, height, batch, _DT[dt], tb_depth, flags, 0)
     p = params or rd_params_default()
     h = C.c_void_p()
@@ -162,6 +163,15 @@ def rd_set_params(h, b: int, params: _lib.rd_params) -> None:
     _check(load().rd_set_params(h, int(b), C.byref(params)), h)
 
 
+def rd_paint_phi(h, b: int, rect, value: float) -> None:
+    r = None if rect is None else C.byref(_lib.rd_rect(*rect))
+    _check(load().rd_paint_phi(h, int(b), r, float(value)), h)
+
+
+def rd_fill_noise(h, b: int = -1, planes: int = 3, seed: int = 1, amplitude: float = 0.1) -> None:
+    _check(load().rd_fill_noise(h, int(b), int(planes), int(seed), float(amplitude)), h)
+
+
 def rd_init_rest(h, b: int = -1) -> None:
     _check(load().rd_init_rest(h, int(b)), h)
 
@@ -203,12 +213,17 @@ def rd_last_error(h) -> str:
 class Sim:
     """Owning wrapper over an rd_sim handle (one instance batch on one GPU)."""
 
-    def __init__(self, phi: np.ndarray, *, dtype=np.float32, tb_depth: int = 0, flags: int = 0,
-                 params=None, pitch: int = 0):
-        phi = np.asarray(phi)
-        if phi.ndim == 2:
-            phi = phi[None]
-        self.B, self.H, self.W = phi.shape
+    def __init__(self, phi: np.ndarray | None = None, *, dtype=np.float32, tb_depth: int = 0, flags: int = 0,
+                 params=None, pitch: int = 0, shape: tuple | None = None):
+        """phi: host map [B][H][W] (or [H][W]); or phi=None with shape=(B, H, W)
+        for phi = 0 on the device (then paint_phi)."""
+        if phi is not None:
+            phi = np.asarray(phi)
+            if phi.ndim == 2:
+                phi = phi[None]
+            self.B, self.H, self.W = phi.shape
+        else:
+            self.B, self.H, self.W = shape
         self.dtype = np.dtype(dtype)
         self.h = rd_create(self.W, self.H, phi, batch=self.B, dtype=dtype, tb_depth=tb_depth, flags=flags,
                            params=params, pitch=pitch)
@@ -262,6 +277,14 @@ class Sim:
     def set_params(self, b: int, params) -> None:
         """Per-instance Eq. 1 parameters (b = -1: all instances)."""
         rd_set_params(self.h, b, params)
+
+    def paint_phi(self, value: float, rect=None, b: int = -1) -> None:
+        """phi := value on rect (y0, x0, y1, x1) or the whole grid (None)."""
+        rd_paint_phi(self.h, b, rect, value)
+
+    def fill_noise(self, b: int = -1, planes: int = 3, seed: int = 1, amplitude: float = 0.1) -> None:
+        """Seeded U[0, amplitude) noise in u/v on the device."""
+        rd_fill_noise(self.h, b, planes, seed, amplitude)
 
     def init_rest(self, b: int = -1) -> None:
         """Quiescent start: u = v = u*(phi) per cell."""

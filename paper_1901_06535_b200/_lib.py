@@ -73,6 +73,8 @@ SYMBOLS = [
     ("rd_probe_result", C.c_int, [P, i32, C.POINTER(C.c_int64)]),
     ("rd_set_params", C.c_int, [P, i32, C.POINTER(rd_params)]),
     ("rd_init_rest", C.c_int, [P, i32]),
+    ("rd_fill_noise", C.c_int, [P, i32, C.c_uint32, C.c_uint64, dbl]),
+    ("rd_paint_phi", C.c_int, [P, i32, C.POINTER(rd_rect), dbl]),
     ("rd_timelapse", C.c_int, [P, i32]),
     ("rd_read_timelapse", C.c_int, [P, i32, P]),
     ("rd_row_ptr", C.c_int, [P, i32, i32, i64, C.POINTER(P), C.POINTER(C.c_int64)]),

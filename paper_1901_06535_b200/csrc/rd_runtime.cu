@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -79,6 +81,13 @@ struct rd_sim {
   int* d_flag = nullptr;
   void* d_scratch = nullptr;  // probe max output
   int num_sms = 148;
+  // CUDA graphs of rd_step segments, keyed by (length, kmax, start buffer,
+  // timelapse sample at the end, arithmetic mode); value: exec graph, number
+  // of stencil launches, kernels launched.
+  std::map<std::tuple<int64_t, int, int, int, int>, std::tuple<cudaGraphExec_t, int64_t, int64_t>> graphs;
+  std::map<std::tuple<int64_t, int, int, int, int>, int> graph_seen;  // capture on the 2nd occurrence
+  cudaStream_t capture_stream = nullptr;
+  bool graphs_broken = false;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   bool profiling = false;
@@ -150,7 +159,7 @@ int auto_tb(const rd_sim* s) {
     int k = atoi(e);
     if (k >= 1 && k <= RD_MAX_TB) return k;
   }
-  return s->esz == 4 ? 4 : 2;
+  return 4;
 }
 
 template <typename T>
@@ -439,6 +448,86 @@ bool probe_due(const rd_sim* s, int64_t step) {
   return false;
 }
 
+// The blocked launches of one segment [s->step, next) (no event or probe
+// inside): direct launches, or -- for non-slab handles in the fast modes --
+// one CUDA graph per distinct segment shape, captured once and replayed, so a
+// small-grid run costs one graph launch per segment instead of two kernel
+// launches per block (the per-launch overhead dominates small batched grids).
+int run_blocks(rd_sim* s, int64_t next, int kmax) {
+  const bool graph = !(s->g.flags & RD_NO_GRAPH) && !s->profiling && !s->slab && !s->precise_mode &&
+                     !s->graphs_broken && next - s->step >= 2 * kmax;
+  if (!graph) {
+    while (s->step < next) {
+      const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      if (int rc = launch_tb(s, k)) return rc;
+      s->step += k;
+    }
+    return RD_OK;
+  }
+  const int tl_end = (s->tl_stride > 0 && next % s->tl_stride == 0) ? 1 : 0;
+  const auto key = std::make_tuple(next - s->step, kmax, s->cur, tl_end, s->fast_mode);
+  auto it = s->graphs.find(key);
+  if (it == s->graphs.end() && ++s->graph_seen[key] < 2) {
+    // first occurrence of this segment shape: launch directly (a one-off
+    // segment would not repay the capture)
+    while (s->step < next) {
+      const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      if (int rc = launch_tb(s, k)) return rc;
+      s->step += k;
+    }
+    return RD_OK;
+  }
+  if (it == s->graphs.end()) {
+    if (!s->capture_stream) RD_CUDA(s, cudaStreamCreateWithFlags(&s->capture_stream, cudaStreamNonBlocking));
+    const int cur0 = s->cur;
+    const int64_t step0 = s->step;
+    const int32_t gv0 = s->ghost_valid;
+    const rd_stats st0 = s->st;
+    cudaStream_t user = s->stream;
+    s->stream = s->capture_stream;
+    cudaGraph_t g = nullptr;
+    int rc = RD_OK;
+    if (cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) rc = RD_ECUDA;
+    while (rc == RD_OK && s->step < next) {
+      const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      rc = launch_tb(s, k);
+      s->step += k;
+    }
+    cudaError_t ec = cudaStreamEndCapture(s->stream, &g);
+    s->stream = user;
+    cudaGraphExec_t ex = nullptr;
+    if (rc == RD_OK && ec == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+      it = s->graphs.emplace(key, std::make_tuple(ex, s->st.step_launches - st0.step_launches,
+                                                   s->st.launches - st0.launches)).first;
+    }
+    if (g) cudaGraphDestroy(g);
+    // rewind the host state advanced by the capture
+    s->cur = cur0;
+    s->step = step0;
+    s->ghost_valid = gv0;
+    s->st = st0;
+    cudaGetLastError();
+    if (it == s->graphs.end()) {  // capture unsupported here: launch directly from now on
+      s->graphs_broken = true;
+      return run_blocks(s, next, kmax);
+    }
+  }
+  const auto& [ex, n_step_launches, n_launches] = it->second;
+  RD_CUDA(s, cudaGraphLaunch(ex, s->stream));
+  if (n_step_launches & 1) s->cur ^= 1;
+  s->st.launches += n_launches;
+  s->st.step_launches += n_step_launches;
+  s->st.cell_updates += s->B * s->H * s->W * (next - s->step);
+  s->step = next;
+  return RD_OK;
+}
+
+void drop_graphs(rd_sim* s) {
+  for (auto& kv : s->graphs) cudaGraphExecDestroy(std::get<0>(kv.second));
+  s->graphs.clear();
+  s->graph_seen.clear();
+}
+
 // Advance from s->step to end with blocks of at most kmax steps.
 int run_range(rd_sim* s, int64_t end, int kmax) {
   int rc = sync_probes(s);
@@ -462,11 +551,7 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
     for (const auto& q : s->probes)
       if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
     if (s->tl_stride > 0) next = std::min(next, (s->step / s->tl_stride + 1) * (int64_t)s->tl_stride);
-    while (s->step < next) {
-      const int k = (int)std::min<int64_t>(kmax, next - s->step);
-      if ((rc = launch_tb(s, k))) return rc;
-      s->step += k;
-    }
+    if ((rc = run_blocks(s, next, kmax))) return rc;
     if (probe_due(s, s->step))
       if ((rc = launch_probes(s, s->step))) return rc;
   }
@@ -586,7 +671,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
                   int64_t Hg, int32_t halo, bool slab, rd_sim** out) {
   if (!out) return set_err(nullptr, RD_EINVAL, "out is NULL");
   *out = nullptr;
-  if (!grid || !params || !phi_host) return set_err(nullptr, RD_EINVAL, "grid, params and phi_map are required");
+  if (!grid || !params) return set_err(nullptr, RD_EINVAL, "grid and params are required");
   if (grid->width < 3 || grid->height < (slab ? 1 : 3))
     return set_err(nullptr, RD_EINVAL, "width and height must be >= 3 (SPEC.md:32)");
   if (grid->batch < 1) return set_err(nullptr, RD_EINVAL, "batch must be >= 1");
@@ -656,7 +741,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   // phi rows present in the host buffer: local [lo, hi)
   const int64_t lo = slab ? std::max<int64_t>(0, row0 - halo) - row0 : 0;
   const int64_t hi = slab ? std::min<int64_t>(Hg, row0 + s->H + halo) - row0 : s->H;
-  for (int64_t b = 0; b < s->B; ++b) {
+  for (int64_t b = 0; b < s->B && phi_host; ++b) {
     const char* src = (const char*)phi_host + (size_t)b * (hi - lo) * s->W * s->esz;
     cudaError_t e = cudaMemcpy2DAsync(plane_ptr(s, s->phi, b, lo), s->pitch * s->esz, src, s->W * s->esz,
                                       s->W * s->esz, hi - lo, cudaMemcpyHostToDevice, s->stream);
@@ -760,6 +845,8 @@ int rd_destroy(rd_sim* s) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
+  drop_graphs(s);
+  if (s->capture_stream) cudaStreamDestroy(s->capture_stream);
   if (s->own_stream) cudaStreamDestroy(s->own_stream);
   delete s;
   return RD_OK;
@@ -978,7 +1065,65 @@ int rd_set_params(rd_sim* s, int32_t b, const rd_params* p) {
     if (s->pinst.empty()) s->pinst.assign((size_t)s->B, s->p);
     s->pinst[(size_t)b] = *p;
   }
+  drop_graphs(s);  // constants are baked into captured launches
   return choose_mode(s);
+}
+
+int rd_paint_phi(rd_sim* s, int32_t b, const rd_rect* r, double value) {
+  if (!s) return RD_EINVAL;
+  if (b < -1 || b >= s->B) return set_err(s, RD_ERANGE, "instance %d out of range", b);
+  if (!std::isfinite(value)) return set_err(s, RD_ENONFINITE, "phi value is not finite");
+  int64_t y0 = 0, y1 = s->Hg, x0 = 0, x1 = s->W;
+  if (r) y0 = r->y0, y1 = r->y1, x0 = r->x0, x1 = r->x1;
+  // global rows -> local rows that this handle stores (owned + ghost rows)
+  const int64_t lo = std::max<int64_t>(std::max<int64_t>(y0, 0) - s->grow0, s->r_lo);
+  const int64_t hi = std::min<int64_t>(std::min<int64_t>(y1, s->Hg) - s->grow0, s->r_hi);
+  x0 = std::max<int64_t>(x0, 0);
+  x1 = std::min<int64_t>(x1, s->W);
+  if (lo < hi && x0 < x1) {
+    const int32_t b0 = b < 0 ? 0 : b, nb = b < 0 ? (int32_t)s->B : 1;
+    const unsigned grid = (unsigned)std::min<int64_t>(((hi - lo) * (x1 - x0) + 255) / 256, s->num_sms * 16);
+    for (int32_t i = b0; i < b0 + nb; ++i) {
+      if (s->esz == 4)
+        rdk::paint_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, s->phi), s->plane_stride, s->pitch,
+                                                              (int32_t)lo, (int32_t)hi, x0, x1, (float)value, i);
+      else
+        rdk::paint_kernel<double><<<grid, 256, 0, s->stream>>>(origin<double>(s, s->phi), s->plane_stride, s->pitch,
+                                                               (int32_t)lo, (int32_t)hi, x0, x1, value, i);
+      RD_CUDA(s, cudaGetLastError());
+      s->st.launches++;
+    }
+  }
+  return launch_mirror(s, s->phi, nullptr, nullptr, s->r_lo, s->r_hi);
+}
+
+int rd_fill_noise(rd_sim* s, int32_t b, uint32_t planes, uint64_t seed, double amplitude) {
+  if (!s) return RD_EINVAL;
+  if (b < -1 || b >= s->B) return set_err(s, RD_ERANGE, "instance %d out of range", b);
+  if (!(planes & 3u) || (planes & ~3u)) return set_err(s, RD_EINVAL, "planes must be a mask of 1 (u) and 2 (v)");
+  if (!std::isfinite(amplitude)) return set_err(s, RD_ENONFINITE, "amplitude is not finite");
+  const int32_t b0 = b < 0 ? 0 : b, nb = b < 0 ? (int32_t)s->B : 1;
+  for (int32_t i = b0; i < b0 + nb; ++i) {
+    for (int p = 0; p < 2; ++p) {
+      if (!(planes & (1u << p))) continue;
+      void* plane = p == 0 ? s->u[s->cur] : s->v[s->cur];
+      const unsigned long long tag = (unsigned long long)p << 62;
+      const unsigned grid = (unsigned)std::min<int64_t>(((s->r_hi - s->r_lo) * s->W + 255) / 256, s->num_sms * 16);
+      if (s->esz == 4)
+        rdk::noise_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, plane), s->plane_stride, s->pitch,
+                                                              s->r_lo, s->r_hi, (int32_t)s->W, s->grow0, seed, tag,
+                                                              amplitude, i);
+      else
+        rdk::noise_kernel<double><<<grid, 256, 0, s->stream>>>(origin<double>(s, plane), s->plane_stride, s->pitch,
+                                                               s->r_lo, s->r_hi, (int32_t)s->W, s->grow0, seed, tag,
+                                                               amplitude, i);
+      RD_CUDA(s, cudaGetLastError());
+      s->st.launches++;
+    }
+  }
+  void* p0 = (planes & 1u) ? s->u[s->cur] : s->v[s->cur];
+  void* p1 = (planes == 3u) ? s->v[s->cur] : nullptr;
+  return launch_mirror(s, p0, p1, nullptr, s->r_lo, s->r_hi);
 }
 
 int rd_init_rest(rd_sim* s, int32_t b) {
@@ -1006,6 +1151,7 @@ int rd_timelapse(rd_sim* s, int32_t stride) {
   if (!s) return RD_EINVAL;
   if (stride < 0) return set_err(s, RD_EINVAL, "stride must be >= 0");
   s->tl_stride = stride;
+  drop_graphs(s);
   if (stride == 0) return RD_OK;
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
   if (!s->tl) {

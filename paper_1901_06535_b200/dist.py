@@ -87,7 +87,9 @@ class SlabSim:
         if self.rows < halo and world > 1:
             raise ValueError("slab thinner than the halo")
         lo, hi = ghost_extent(H, self.row0, self.rows, halo)
-        phi = np.stack([np.ascontiguousarray(phi_fn(b, lo, hi - lo), dtype=dtype) for b in range(batch)])
+        # phi_fn(b, row0, rows) -> host rows, or None: phi = 0 (paint on the device)
+        phi = (None if phi_fn is None else
+               np.stack([np.ascontiguousarray(phi_fn(b, lo, hi - lo), dtype=dtype) for b in range(batch)]))
         self.dtype = np.dtype(dtype)
         self.batch = batch
         self.h = rd_create_slab(W, self.rows, phi, self.row0, H, halo, batch=batch, dtype=dtype,
@@ -116,6 +118,11 @@ class SlabSim:
         u = np.ascontiguousarray(u_fn(b, self.row0, self.rows), dtype=self.dtype)
         v = None if v_fn is None else np.ascontiguousarray(v_fn(b, self.row0, self.rows), dtype=self.dtype)
         rd_write_fields(self.h, b, u, v)
+
+    def fill_noise(self, b: int = -1, planes: int = 3, seed: int = 1, amplitude: float = 0.1):
+        """Global-coordinate noise on the device, ghost rows included."""
+        from . import rd_fill_noise
+        rd_fill_noise(self.h, b, planes, seed, amplitude)
 
     def stimulate(self, shape: dict, value: float = 1.0, at_step: int = 0, b: int = -1):
         rd_stimulate(self.h, b, shape, value, at_step)  # global coordinates; the slab clips

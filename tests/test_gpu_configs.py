@@ -81,3 +81,25 @@ def test_config5_crop_bitwise():
     r = oracle_run(w, 0)
     assert_bitwise(U[0], r.u, "u")
     assert_bitwise(V[0], r.v, "v")
+
+
+def test_config5_device_built_crop_bitwise():
+    """configs[4] built on the device (rd_paint_phi background + obstacles,
+    rd_fill_noise, masked half-discs) on a 2048^2 crop equals the oracle on
+    the rdinputs host inputs, bitwise, after 30 steps."""
+    import paper_1901_06535_b200 as rd
+    import oracle
+    w = config(5, H=2048, W=2048, steps=30, n_obstacles=24)
+    sim = rd.Sim(None, shape=(1, w.H, w.W), dtype=np.float32)
+    sim.paint_phi(0.054)
+    for (y0, x0, y1, x1) in w.meta["obstacles"]:
+        sim.paint_phi(0.2, (y0, x0, y1, x1))
+    sim.fill_noise(seed=1)
+    for s, val, at in w.events[0]:
+        sim.stimulate(s, val, at)
+    sim.step(w.steps)
+    u, v = sim.read(0)
+    sim.close()
+    r = oracle_run(w, 0)
+    assert_bitwise(u, r.u, "u")
+    assert_bitwise(v, r.v, "v")

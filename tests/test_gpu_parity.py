@@ -287,3 +287,38 @@ def test_rest_init_and_spiral_seeding(dtype):
     assert_bitwise(u, ref.u, "u")
     assert_bitwise(v, ref.v, "v")
     assert (u > 0.1).mean() > 0.05
+
+
+@pytest.mark.parametrize("dtype", DT, ids=IDS)
+def test_graph_replay_equals_direct_launches(dtype):
+    """CUDA-graph replay of rd_step segments (default) and direct launches
+    (RD_NO_GRAPH) give bitwise identical fields and probe latches."""
+    from rdinputs import config
+    w = config(2, dtype=dtype, steps=1500)
+    Ug, Vg, Fg, sg = gpu_run(w)
+    Ud, Vd, Fd, sd = gpu_run(w, flags=rd.RD_NO_GRAPH)
+    assert_bitwise(Ug, Ud, "u")
+    assert_bitwise(Vg, Vd, "v")
+    assert Fg == Fd
+    assert sg["step_launches"] == sd["step_launches"]
+
+
+@pytest.mark.parametrize("dtype", DT, ids=IDS)
+def test_device_noise_equals_rdinputs(dtype):
+    """rd_fill_noise (device SplitMix64) equals rdinputs.noise_plane bitwise,
+    for a full grid and for a slab with a global row offset."""
+    H, W = 77, 301
+    sim = rd.Sim(np.full((H, W), 0.054, dtype=dtype), dtype=dtype)
+    sim.fill_noise(seed=1)
+    u, v = sim.read(0)
+    sim.close()
+    assert_bitwise(u, noise_plane(H, W, 0, seed=1, dtype=dtype), "u")
+    assert_bitwise(v, noise_plane(H, W, 1, seed=1, dtype=dtype), "v")
+    h = rd.rd_create_slab(W, 20, np.full((28, W), 0.054, dtype=dtype), 40, H, 4, dtype=dtype)
+    rd.rd_fill_noise(h, -1, 3, 9, 0.1)
+    us = np.empty((20, W), dtype)
+    vs = np.empty((20, W), dtype)
+    rd.rd_read_fields(h, 0, us, vs)
+    rd.rd_destroy(h)
+    assert_bitwise(us, noise_plane(20, W, 0, seed=9, dtype=dtype, row0=40, W_global=W), "u slab")
+    assert_bitwise(vs, noise_plane(20, W, 1, seed=9, dtype=dtype, row0=40, W_global=W), "v slab")
