@@ -185,6 +185,23 @@ int rd_stimulate(struct rd_sim* sim, int32_t b, const rd_shape* shape, double va
  * is bitwise identical to rd_step(a+b). */
 int rd_step(struct rd_sim* sim, int64_t n);
 
+/* Deferred health checking (slab super-steps): a checkpoint,
+ * any number of unchecked blocks, one flag read, and -- if a flag is set --
+ * restore + an exact step-by-step rd_step replay by the caller.
+ *   rd_checkpoint      save u, v, probe latches, timelapse, step and pending
+ *                      stimuli (async on the stream; RD_EINVAL with
+ *                      RD_NO_CHECKPOINT).
+ *   rd_step_unchecked  advance n steps with the fast kernels: no checkpoint,
+ *                      no flag read, no host synchronisation.
+ *   rd_read_flags      sync; *nonfinite = a non-finite cell was produced,
+ *                      *inexact = the fast division's guard tripped (results
+ *                      since the checkpoint must be replayed); clears both.
+ *   rd_restore         return to the last checkpoint. */
+int rd_checkpoint(struct rd_sim* sim);
+int rd_step_unchecked(struct rd_sim* sim, int64_t n);
+int rd_read_flags(struct rd_sim* sim, int32_t* nonfinite, int32_t* inexact);
+int rd_restore(struct rd_sim* sim);
+
 int64_t rd_get_step(const struct rd_sim* sim);
 int rd_get_fault(const struct rd_sim* sim, rd_fault* out);
 

@@ -21,7 +21,7 @@ from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_C
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
-           "rd_get_step", "rd_get_fault", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
+           "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -109,6 +109,24 @@ def rd_stimulate(h, b: int, shape: dict, value: float = 1.0, at_step: int = 0) -
 
 def rd_step(h, n: int) -> None:
     _check(load().rd_step(h, int(n)), h)
+
+
+def rd_checkpoint(h) -> None:
+    _check(load().rd_checkpoint(h), h)
+
+
+def rd_step_unchecked(h, n: int) -> None:
+    _check(load().rd_step_unchecked(h, int(n)), h)
+
+
+def rd_read_flags(h) -> tuple[bool, bool]:
+    nf, ie = C.c_int32(), C.c_int32()
+    _check(load().rd_read_flags(h, C.byref(nf), C.byref(ie)), h)
+    return bool(nf.value), bool(ie.value)
+
+
+def rd_restore(h) -> None:
+    _check(load().rd_restore(h), h)
 
 
 def rd_get_step(h) -> int:

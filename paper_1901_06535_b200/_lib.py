@@ -66,6 +66,10 @@ SYMBOLS = [
     ("rd_write_fields_device", C.c_int, [P, i32, P, P]),
     ("rd_stimulate", C.c_int, [P, i32, C.POINTER(rd_shape), dbl, i64]),
     ("rd_step", C.c_int, [P, i64]),
+    ("rd_checkpoint", C.c_int, [P]),
+    ("rd_step_unchecked", C.c_int, [P, i64]),
+    ("rd_read_flags", C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    ("rd_restore", C.c_int, [P]),
     ("rd_get_step", C.c_int64, [P]),
     ("rd_get_fault", C.c_int, [P, C.POINTER(rd_fault)]),
     ("rd_probe", C.c_int, [P, i32, C.POINTER(rd_rect), dbl, C.POINTER(C.c_int32), C.POINTER(C.c_double)]),

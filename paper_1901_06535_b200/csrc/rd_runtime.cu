@@ -64,6 +64,11 @@ struct rd_sim {
   void* tl = nullptr;     // f2: timelapse max_u planes
   void* ck_tl = nullptr;
   int32_t tl_stride = 0;
+  // host side of the checkpoint (device side: ck_u, ck_v, d_first_ck, ck_tl)
+  int64_t ck_step = 0;
+  int ck_cur = 0;
+  std::vector<PendingEvent> ck_events;
+  bool ck_valid = false;
   int cur = 0;
   int64_t step = 0;
   int32_t ghost_valid = 0;  // slab: ghost rows still valid in the current buffers
@@ -574,6 +579,40 @@ int reset_fault(rd_sim* s) {
   return RD_OK;
 }
 
+// Checkpoint = u, v (current buffers), probe latches, timelapse, step,
+// buffer parity and pending events; restore returns to it exactly.
+int save_checkpoint(rd_sim* s) {
+  if (!s->ck_u) return set_err(s, RD_EINVAL, "handle created with RD_NO_CHECKPOINT");
+  const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
+  RD_CUDA(s, cudaMemcpyAsync(s->ck_u, s->u[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
+  RD_CUDA(s, cudaMemcpyAsync(s->ck_v, s->v[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
+  if (!s->probes.empty())
+    RD_CUDA(s, cudaMemcpyAsync(s->d_first_ck, s->d_first, sizeof(long long) * s->probes.size(),
+                               cudaMemcpyDeviceToDevice, s->stream));
+  if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->ck_tl, s->tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
+  s->ck_step = s->step;
+  s->ck_cur = s->cur;
+  s->ck_events = s->events;
+  s->ck_valid = true;
+  return RD_OK;
+}
+
+int restore_checkpoint(rd_sim* s) {
+  if (!s->ck_valid) return set_err(s, RD_ERANGE, "no checkpoint to restore");
+  const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
+  s->cur = s->ck_cur;
+  RD_CUDA(s, cudaMemcpyAsync(s->u[s->cur], s->ck_u, bytes, cudaMemcpyDeviceToDevice, s->stream));
+  RD_CUDA(s, cudaMemcpyAsync(s->v[s->cur], s->ck_v, bytes, cudaMemcpyDeviceToDevice, s->stream));
+  if (!s->probes.empty())
+    RD_CUDA(s, cudaMemcpyAsync(s->d_first, s->d_first_ck, sizeof(long long) * s->probes.size(),
+                               cudaMemcpyDeviceToDevice, s->stream));
+  if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->tl, s->ck_tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
+  s->events = s->ck_events;
+  s->step = s->ck_step;
+  s->ghost_valid = (int32_t)s->halo;
+  return reset_fault(s);
+}
+
 int alloc_planes(rd_sim* s) {
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
   void** ps[5] = {&s->u[0], &s->u[1], &s->v[0], &s->v[1], &s->phi};
@@ -921,20 +960,9 @@ int rd_step(rd_sim* s, int64_t n) {
   s->ghost_valid = (int32_t)s->halo;
   const bool ckpt = !(s->g.flags & RD_NO_CHECKPOINT);
   const int64_t step0 = s->step;
-  const int cur0 = s->cur;
-  std::vector<PendingEvent> events0;
   int rc = sync_probes(s);
   if (rc) return rc;
-  if (ckpt) {
-    const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
-    RD_CUDA(s, cudaMemcpyAsync(s->ck_u, s->u[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
-    RD_CUDA(s, cudaMemcpyAsync(s->ck_v, s->v[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
-    if (!s->probes.empty())
-      RD_CUDA(s, cudaMemcpyAsync(s->d_first_ck, s->d_first, sizeof(long long) * s->probes.size(),
-                                 cudaMemcpyDeviceToDevice, s->stream));
-    if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->ck_tl, s->tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
-    events0 = s->events;
-  }
+  if (ckpt && (rc = save_checkpoint(s))) return rc;
   if ((rc = run_range(s, step0 + n, s->K))) return rc;
   unsigned long long key = ~0ull;
   int precise_hit = 0;
@@ -946,18 +974,7 @@ int rd_step(rd_sim* s, int64_t n) {
     // per launch, checking for non-finite cells after every step: the handle
     // ends at the first failing step (or at step0+n), bit-identical to a
     // step-by-step exact run (results do not depend on the blocking depth).
-    const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
-    s->cur = cur0;
-    RD_CUDA(s, cudaMemcpyAsync(s->u[s->cur], s->ck_u, bytes, cudaMemcpyDeviceToDevice, s->stream));
-    RD_CUDA(s, cudaMemcpyAsync(s->v[s->cur], s->ck_v, bytes, cudaMemcpyDeviceToDevice, s->stream));
-    if (!s->probes.empty())
-      RD_CUDA(s, cudaMemcpyAsync(s->d_first, s->d_first_ck, sizeof(long long) * s->probes.size(),
-                                 cudaMemcpyDeviceToDevice, s->stream));
-    if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->tl, s->ck_tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
-    s->events = events0;
-    s->step = step0;
-    s->ghost_valid = (int32_t)s->halo;
-    if ((rc = reset_fault(s))) return rc;
+    if ((rc = restore_checkpoint(s))) return rc;
     key = ~0ull;
     s->precise_mode = true;
     s->st.replays++;
@@ -984,6 +1001,37 @@ int rd_step(rd_sim* s, int64_t n) {
   return set_err(s, RD_ENONFINITE, "non-finite value at instance %d, cell (%lld, %lld) after step %lld%s", s->fault.b,
                  (long long)s->fault.i, (long long)s->fault.j, (long long)s->fault.step,
                  ckpt ? "" : " (k-block granularity: RD_NO_CHECKPOINT)");
+}
+
+int rd_step_unchecked(rd_sim* s, int64_t n) {
+  if (!s) return RD_EINVAL;
+  if (n < 0) return set_err(s, RD_EINVAL, "n must be >= 0");
+  if (s->slab && n > s->halo) return set_err(s, RD_ERANGE, "slab handles step at most halo=%lld steps per call", (long long)s->halo);
+  if (n == 0) return RD_OK;
+  s->ghost_valid = (int32_t)s->halo;
+  if (int rc = sync_probes(s)) return rc;
+  return run_range(s, s->step + n, s->K);
+}
+
+int rd_checkpoint(rd_sim* s) {
+  if (!s) return RD_EINVAL;
+  if (int rc = sync_probes(s)) return rc;
+  return save_checkpoint(s);
+}
+
+int rd_restore(rd_sim* s) {
+  if (!s) return RD_EINVAL;
+  return restore_checkpoint(s);
+}
+
+int rd_read_flags(rd_sim* s, int32_t* nonfinite, int32_t* inexact) {
+  if (!s) return RD_EINVAL;
+  unsigned long long key = ~0ull;
+  int p = 0;
+  if (int rc = read_fault(s, &key, &p)) return rc;
+  if (nonfinite) *nonfinite = key != ~0ull;
+  if (inexact) *inexact = p != 0;
+  return reset_fault(s);
 }
 
 int64_t rd_get_step(const rd_sim* s) { return s ? s->step : -1; }

@@ -17,8 +17,9 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import rd_create_slab, rd_destroy, rd_get_stats, rd_probe_latch, rd_probe_result, rd_read_fields
-from . import rd_row_ptr, rd_set_stream, rd_step, rd_stimulate, rd_write_fields
+from . import RD_ENONFINITE, RDError, rd_checkpoint, rd_create_slab, rd_destroy, rd_get_stats, rd_probe_latch
+from . import rd_probe_result, rd_read_fields, rd_read_flags, rd_restore, rd_row_ptr, rd_set_stream, rd_step
+from . import rd_step_unchecked, rd_stimulate, rd_write_fields
 
 
 def slab_rows(H: int, world: int, rank: int) -> tuple[int, int]:
@@ -151,14 +152,48 @@ class SlabSim:
         else:
             self.transport.exchange(self)
 
+    def any_rank(self, flag: bool) -> bool:
+        """Logical OR of a flag over all ranks (MAX all-reduce)."""
+        if self.world == 1:
+            return bool(flag)
+        import torch
+        import torch.distributed as dist
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return bool(t.item())
+
     def step(self, n: int):
-        """Advance n steps: blocks of <= halo steps, each preceded by a halo
-        exchange (so ghosts are fresh after writes, too)."""
-        while n > 0:
-            k = min(self.halo, n)
+        """Advance n steps as one super-step: checkpoint; blocks of <= halo
+        steps, each preceded by a halo exchange, with no host synchronisation;
+        one flag read OR-reduced over ranks. If any rank produced a non-finite
+        cell or tripped the fast-division guard, every rank restores and
+        replays step by step (exchange + exact rd_step(1)), all stopping at the
+        first failing step, which raises RD_ENONFINITE on every rank."""
+        if n <= 0:
+            return
+        rd_checkpoint(self.h)
+        done = 0
+        while done < n:
+            k = min(self.halo, n - done)
             self.exchange()
-            rd_step(self.h, k)
-            n -= k
+            rd_step_unchecked(self.h, k)
+            done += k
+        nonfinite, inexact = rd_read_flags(self.h)
+        if not self.any_rank(nonfinite or inexact):
+            return
+        rd_restore(self.h)
+        for _ in range(n):
+            self.exchange()
+            err = None
+            try:
+                rd_step(self.h, 1)
+            except RDError as e:
+                if e.code != RD_ENONFINITE:
+                    raise
+                err = e
+            if self.any_rank(err is not None):
+                raise err or RDError(RD_ENONFINITE, "non-finite value produced on another rank")
 
     def read_owned(self, b: int = 0):
         u = np.empty((self.rows, self.W), dtype=self.dtype)
@@ -200,11 +235,35 @@ class LoopbackGroup:
         torch.cuda.synchronize()  # the engine's streams are non-blocking
 
     def step_all(self, n: int):
-        halo = self.slabs[0].halo
-        while n > 0:
-            k = min(halo, n)
-            for r in range(self.world):
-                self.slabs[r].exchange()
-            for r in range(self.world):
-                rd_step(self.slabs[r].h, k)
-            n -= k
+        """The SlabSim.step super-step protocol over all virtual ranks."""
+        if n <= 0:
+            return
+        slabs = [self.slabs[r] for r in range(self.world)]
+        halo = slabs[0].halo
+        for sl in slabs:
+            rd_checkpoint(sl.h)
+        done = 0
+        while done < n:
+            k = min(halo, n - done)
+            for sl in slabs:
+                sl.exchange()
+            for sl in slabs:
+                rd_step_unchecked(sl.h, k)
+            done += k
+        if not any(any(rd_read_flags(sl.h)) for sl in slabs):
+            return
+        for sl in slabs:
+            rd_restore(sl.h)
+        for _ in range(n):
+            for sl in slabs:
+                sl.exchange()
+            errs = []
+            for sl in slabs:
+                try:
+                    rd_step(sl.h, 1)
+                except RDError as e:
+                    if e.code != RD_ENONFINITE:
+                        raise
+                    errs.append(e)
+            if errs:
+                raise errs[0]

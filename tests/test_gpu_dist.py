@@ -60,3 +60,41 @@ def test_virtual_slabs_equal_single_grid(G, halo, dtype):
     u1, v1 = sim.read(0)
     sim.close()
     assert_bitwise(U, u1, "u single")
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_virtual_slabs_fault_and_guard_replay(G):
+    """Super-step protocol: an unmasked stimulus inside a phi=0.2 obstacle on
+    noisy u,v diverges; the slabs detect it, restore, replay step by step and
+    stop at the oracle's failing step, reporting the oracle's first cell (in
+    global coordinates) with identical fields."""
+    H, W, steps = 96, 128, 400
+    dtype = np.float32
+
+    def phi_fn(b, row0, rows):
+        return np.full((rows, W), 0.2)
+
+    def u_fn(b, row0, rows):
+        return noise_plane(rows, W, 0, seed=7, dtype=dtype, row0=row0)
+
+    def v_fn(b, row0, rows):
+        return noise_plane(rows, W, 1, seed=7, dtype=dtype, row0=row0)
+
+    shape = {"kind": "half_disc", "cy2": 2 * 47, "cx2": 128, "r": 8, "dir": 1}  # straddles the slab edge
+    ref = oracle.run(u_fn(0, 0, H), v_fn(0, 0, H), phi_fn(0, 0, H).astype(dtype), steps, events=[(shape, 1.0, 0)])
+    assert ref.status == -4
+    grp = LoopbackGroup(G)
+    slabs = [SlabSim(W, H, r, G, phi_fn, dtype=dtype, halo=4, transport=grp) for r in range(G)]
+    for s in slabs:
+        s.write(0, u_fn, v_fn)
+        s.stimulate(shape, 1.0, 0)
+    with pytest.raises(rd.RDError) as e:
+        grp.step_all(steps)
+    assert e.value.code == rd.RD_ENONFINITE
+    faults = [rd.rd_get_fault(s.h) for s in slabs if rd.rd_get_fault(s.h)[0] > 0]
+    assert faults and min((f[0], f[2], f[3]) for f in faults) == ref.fault
+    U = np.concatenate([s.read_owned(0)[0] for s in slabs])
+    assert_bitwise(U, ref.u, "u at fault")
+    assert all(rd.rd_get_step(s.h) == ref.fault[0] for s in slabs)
+    for s in slabs:
+        s.close()
