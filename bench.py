@@ -146,7 +146,7 @@ def run_ours(args):
         workload = {"workload": f"configs[4] weak scaling: ({H})x{W} fp32 row slabs, 16 obstacles/GPU phi=0.2, "
                                 "masked half-discs, NCCL halo exchange", "grid": [H, W]}
     stream = torch.cuda.current_stream()
-    rd.rd_set_stream(h, stream.cuda_stream)
+    rd.rd_set_stream(h, rd.stream_handle(stream))  # engine work on the stream the events are recorded on
 
     def barrier():
         torch.cuda.synchronize()

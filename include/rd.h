@@ -151,7 +151,8 @@ int rd_create(const rd_grid* grid, const rd_params* params, const void* phi_map,
 int rd_destroy(struct rd_sim* sim);
 
 /* Use an external CUDA stream (cudaStream_t, e.g. torch's current stream)
- * for all subsequent work; NULL reverts to the handle's own stream. */
+ * for all subsequent work; NULL reverts to the handle's own (non-blocking)
+ * stream. To share the legacy default stream pass cudaStreamLegacy (0x1). */
 int rd_set_stream(struct rd_sim* sim, void* cuda_stream);
 
 /* ---- state I/O (HOST buffers, [height][width] of dtype, row-major) ---- */

@@ -21,7 +21,7 @@ from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_C
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
-           "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
+           "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -98,7 +98,19 @@ def rd_destroy(h) -> None:
     _check(load().rd_destroy(h), h)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream as an explicit handle
+
+
+def stream_handle(stream) -> int:
+    """cudaStream_t of a torch.cuda.Stream (or an int). torch's default stream
+    reports handle 0, which rd_set_stream would read as "the handle's own
+    stream": map it to cudaStreamLegacy so the engine really shares it."""
+    ptr = int(getattr(stream, "cuda_stream", stream) or 0)
+    return ptr if ptr else CUDA_STREAM_LEGACY
+
+
 def rd_set_stream(h, stream_ptr: int | None) -> None:
+    """stream_ptr: a cudaStream_t (int), None = the handle's own stream."""
     _check(load().rd_set_stream(h, C.c_void_p(stream_ptr) if stream_ptr else None), h)
 
 
@@ -321,8 +333,7 @@ class Sim:
 
     def set_stream(self, stream) -> None:
         """Issue work on a torch.cuda.Stream (or raw cudaStream_t int)."""
-        ptr = getattr(stream, "cuda_stream", stream)
-        rd_set_stream(self.h, ptr)
+        rd_set_stream(self.h, stream_handle(stream))
 
     def stats(self) -> dict:
         return rd_get_stats(self.h)

@@ -48,17 +48,28 @@ def exchange_plan(world: int, rank: int, rows: int, halo: int):
 
 def exchange(tensors_by_peer, group=None):
     """One halo exchange: tensors_by_peer = [(peer, [send...], [recv...])].
-    All sends/recvs are posted as one batch (NCCL group) and waited on."""
+    All sends/recvs are posted as one batch (an NCCL group) and waited on.
+    With NCCL, device rows go GPU to GPU over NVLink; with a CPU backend
+    (gloo: tests) device rows are staged through host tensors."""
+    import torch
     import torch.distributed as dist
+    staged = dist.get_backend(group) != "nccl" and any(
+        t.is_cuda for _, ss, rs in tensors_by_peer for t in list(ss) + list(rs))
+    landing = []
     ops = []
     for peer, sends, recvs in tensors_by_peer:
         for s in sends:
-            ops.append(dist.P2POp(dist.isend, s, peer, group))
+            ops.append(dist.P2POp(dist.isend, s.cpu() if staged else s, peer, group))
         for r in recvs:
-            ops.append(dist.P2POp(dist.irecv, r, peer, group))
+            buf = torch.empty(r.shape, dtype=r.dtype) if staged else r
+            if staged:
+                landing.append((buf, r))
+            ops.append(dist.P2POp(dist.irecv, buf, peer, group))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
+    for buf, r in landing:
+        r.copy_(buf)
 
 
 class _DevRows:
@@ -112,7 +123,8 @@ class SlabSim:
             self.h = None
 
     def set_stream(self, stream):
-        rd_set_stream(self.h, getattr(stream, "cuda_stream", stream))
+        from . import stream_handle
+        rd_set_stream(self.h, stream_handle(stream))
 
     def write(self, b: int, u_fn, v_fn=None):
         """Write owned rows from global-row generators u_fn(b, row0, rows)."""
