@@ -212,7 +212,7 @@ int launch_mirror(rd_sim* s, void* p0, void* p1, void* p2, int32_t x_lo, int32_t
   const int nplanes = p2 ? 3 : (p1 ? 2 : 1);
   const int64_t cells = (int64_t)(x_hi - x_lo + 2 * rdk::kMarginRows) * 2 * rdk::kMarginCols +
                         (int64_t)2 * rdk::kMarginRows * s->W;
-  const unsigned bx = (unsigned)std::min<int64_t>((cells + 255) / 256, 4 * s->num_sms);
+  const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((cells + 255) / 256, 4 * s->num_sms));
   dim3 grid(bx, (unsigned)(nplanes * s->B));
   if (s->esz == 4)
     rdk::mirror_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, p0), p1 ? origin<float>(s, p1) : nullptr,
