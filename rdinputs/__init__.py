@@ -8,7 +8,7 @@ struct; membership of a shape is computed by each side independently.
 """
 from .gen import splitmix64, stream, noise_plane, half_discs, obstacles  # noqa: F401
 from .geometry import and_gate, diode, phi_from_rects  # noqa: F401
-from .workloads import Workload, config, spiral_seed  # noqa: F401
+from .workloads import PRESET_PX, Workload, barrier, config, preset_cells, spiral_seed  # noqa: F401
 
 PHI_ACTIVE = 0.054   # Table 1
 PHI_PASSIVE = 0.0975  # Table 1

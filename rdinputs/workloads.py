@@ -130,6 +130,45 @@ def spiral_seed(dtype=np.float64, steps=40000, H=160, W=160, delay=3500, offset=
     return Workload("f4_spiral" if staggered else "f4_target", H, W, 1, dtype, steps, [phi], [ev], rest_init=True)
 
 
+PRESET_PX = {"permeable": 2, "semi_permeable": 3, "impermeable": 8}
+
+
+def preset_cells(px: int) -> int:
+    """Barrier width in cells for a preset in display pixels: the 400x300
+    simulation is shown at 800x600, so px/2 cells, a half cell
+    rounded up (R-21): 2 px -> 1, 3 px -> 2, 8 px -> 4."""
+    return (px + 1) // 2
+
+
+def barrier(preset: str, incidence: str, dtype=np.float64, steps=16000, H=120, W=200, x0=100, cap=30,
+            phi_passive=0.0975) -> Workload:
+    """f3: a straight line of inhibitive substrate
+    (phi_passive, Table 1) of the preset's width along the whole height at
+    column x0, in an otherwise active medium.
+      incidence="perpendicular": a plane wave launched from the left edge hits
+        the line head-on; the probe sits 30 columns past it.
+      incidence="parallel": a plane wave launched along the top rows travels
+        down, sliding along the line (front perpendicular to it); the first
+        `cap` rows of the line are made impermeable (12 cells of phi=0.2) so
+        the launch itself does not touch the line; the probe watches the far
+        side below the cap.
+      preset=None: no line (the control)."""
+    w = preset_cells(PRESET_PX[preset]) if preset else 0
+    phi = np.full((H, W), 0.054)
+    if w:
+        phi[:, x0:x0 + w] = phi_passive
+    if incidence == "perpendicular":
+        ev = [({"kind": "rect", "y0": 0, "x0": 0, "y1": H, "x1": 4}, 1.0, 0)]
+        pr = [((H // 2 - 10, x0 + 30, H // 2 + 10, x0 + 32), PROBE_THRESHOLD, PROBE_STRIDE)]
+    else:
+        if w:
+            phi[:cap, x0:x0 + 12] = 0.2
+        ev = [({"kind": "rect", "y0": 0, "x0": 0, "y1": 4, "x1": x0}, 1.0, 0)]
+        pr = [((cap + 10, x0 + 14, H, x0 + 16), PROBE_THRESHOLD, PROBE_STRIDE)]
+    return Workload(f"f3_{preset or 'control'}_{incidence}", H, W, 1, dtype, steps, [phi], [ev], [pr],
+                    meta={"width_cells": w})
+
+
 _CFGS = {1: _cfg1, 2: _cfg2, 3: _cfg3, 4: _cfg4, 5: _cfg5}
 
 
@@ -139,4 +178,4 @@ def config(n: int, **kw) -> Workload:
     return _CFGS[n](**kw)
 
 
-__all__ = ["Workload", "config", "phi_from_rects", "spiral_seed"]
+__all__ = ["Workload", "config", "phi_from_rects", "spiral_seed", "barrier", "preset_cells", "PRESET_PX"]

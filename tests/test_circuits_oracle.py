@@ -98,3 +98,36 @@ def test_staggered_stimuli_sustain_activity():
     c = spiral_seed(staggered=False, steps=12000)
     r1 = oracle.run(u, v, c.phi_plane(0), c.steps, events=c.events[0])
     assert r1.u.max() < 0.01
+
+
+@pytest.fixture(scope="module")
+def barrier_runs():
+    from rdinputs import barrier
+    out = {}
+    for preset in (None, "permeable", "semi_permeable", "impermeable"):
+        for inc in ("perpendicular", "parallel"):
+            if preset is None and inc == "parallel":
+                continue
+            w = barrier(preset, inc)
+            z = np.zeros((w.H, w.W))
+            out[(preset, inc)] = oracle.run(z, z, w.phi_plane(0), w.steps, events=w.events[0],
+                                            probes=w.probes[0]).first_fire[0]
+    return out
+
+
+def test_permeability_presets(barrier_runs):
+    """f3: with Table 1's phi_passive and the preset widths
+    read as display pixels at 2x (R-21: 1, 2, 4 cells), a permeable line slows
+    a perpendicular wave and lets both through; a semi-permeable line passes
+    the perpendicular wave and blocks the parallel one; an impermeable line
+    blocks both."""
+    want = golden("paper_outcomes.json")["permeability_presets"]
+    ctrl = barrier_runs[(None, "perpendicular")]
+    assert ctrl > 0
+    for preset in ("permeable", "semi_permeable", "impermeable"):
+        perp = barrier_runs[(preset, "perpendicular")]
+        par = barrier_runs[(preset, "parallel")]
+        assert (perp >= 0) == want[preset]["perpendicular"], preset
+        assert (par >= 0) == want[preset]["parallel"], preset
+        if want[preset].get("delayed"):
+            assert perp > ctrl
