@@ -103,3 +103,31 @@ def test_config5_device_built_crop_bitwise():
     r = oracle_run(w, 0)
     assert_bitwise(u, r.u, "u")
     assert_bitwise(v, r.v, "v")
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
+def test_permeability_presets_batched(dtype):
+    """f3: the seven barrier runs (control + 3 presets x 2 incidences) as ONE
+    batched handle (per-instance phi maps); fields and probe latches bitwise
+    equal to the oracle, outcomes as P:163-168 describes."""
+    import oracle
+    from helpers import golden
+    from rdinputs import barrier
+    from rdinputs.workloads import Workload
+    runs = [(None, "perpendicular")] + [(p, i) for p in ("permeable", "semi_permeable", "impermeable")
+                                        for i in ("perpendicular", "parallel")]
+    ws = [barrier(p, i, dtype=dtype) for p, i in runs]
+    w = Workload("f3_batch", ws[0].H, ws[0].W, len(ws), dtype, ws[0].steps, [x.phi[0] for x in ws],
+                 [x.events[0] for x in ws], [x.probes[0] for x in ws])
+    U, V, fire, _ = gpu_run(w)
+    res = {}
+    for b, (p, i) in enumerate(runs):
+        r = oracle_run(w, b)
+        assert fire[b] == r.first_fire
+        assert_bitwise(U[b], r.u, f"u {p} {i}")
+        res[(p, i)] = fire[b][0]
+    want = golden("paper_outcomes.json")["permeability_presets"]
+    for p in ("permeable", "semi_permeable", "impermeable"):
+        assert (res[(p, "perpendicular")] >= 0) == want[p]["perpendicular"]
+        assert (res[(p, "parallel")] >= 0) == want[p]["parallel"]
+    assert res[("permeable", "perpendicular")] > res[(None, "perpendicular")]
