@@ -51,7 +51,11 @@ struct rd_sim {
   int32_t margin = 0;   // ghost rows above/below (slab halo or mirror margin)
   std::vector<rd_params> pinst;  // f1: per-instance parameters (empty = all use p)
   int64_t div4_mismatches = -1;  // result of the 4-op division certification (-1: not run)
-  int fast_mode = 0;    // rdk::MODE_FOLD[_DIV4] when 1/dx^2 is a power of two, else MODE_PRECISE
+  int fast_mode = 0;
+  bool use_lp = false;  // level-parallel kernel (opt-in: RD_KERNEL=lp)
+  bool use_cr = false;  // a8 cluster-resident kernel (small instances, one wave)
+  int cr_cs = 0;        // CTAs per cluster for cr_kernel
+  size_t cr_smem = 0;   // its dynamic shared memory per CTA
   int64_t grow0 = 0, Hg = 0;
   bool slab = false;
   int top_edge = 1, bot_edge = 1;
@@ -229,11 +233,10 @@ int launch_mirror(rd_sim* s, void* p0, void* p1, void* p2, int32_t x_lo, int32_t
   return RD_OK;
 }
 
-template <typename T, int K, bool REACT, int MODE>
-cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_hi) {
-  constexpr int V = vec_of<T>();
-  using G = rdk::StripGeom<K, V>;
-  rdk::TBArgs<T> a;
+// Kernel arguments common to both stencil kernels (everything but the task
+// geometry and row-block height).
+template <typename T>
+void fill_args(rd_sim* s, rdk::TBArgs<T>& a, int in, int out, int32_t out_lo, int32_t out_hi, int K) {
   a.u_in = origin<T>(s, s->u[in]);
   a.v_in = origin<T>(s, s->v[in]);
   a.phi = origin<T>(s, s->phi);
@@ -245,18 +248,6 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_
   a.W = (int32_t)s->W;
   a.out_lo = out_lo;
   a.out_hi = out_hi;
-  a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
-  // persistent grid of one-warp CTAs: as many as can be resident (occupancy
-  // API), capped by the number of tasks
-  static int per_sm = 0;
-  if (!per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdk::tb_kernel<T, K, V, REACT, MODE>, 32, 0) !=
-            cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-  }
-  const int64_t ctas = (int64_t)s->num_sms * per_sm;
-  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, K, ctas);
   a.batch = (int32_t)s->B;
   a.pad_ = 0;
   a.grow0 = s->grow0;
@@ -271,14 +262,64 @@ cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_
   a.fault_key = s->d_fault;
   a.precise_flag = s->d_precise;
   a.tl = (s->tl_stride > 0 && (s->step + K) % s->tl_stride == 0) ? origin<T>(s, s->tl) : nullptr;
+}
+
+template <typename T, int K, bool REACT, int MODE>
+cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_hi) {
+  constexpr int V = vec_of<T>();
+  using G = rdk::StripGeom<K, V>;
+  rdk::TBArgs<T> a;
+  fill_args<T>(s, a, in, out, out_lo, out_hi, K);
+  a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
+  // persistent grid of one-warp CTAs: as many as can be resident (occupancy
+  // API), capped by the number of tasks
+  static int per_sm = 0;
+  if (!per_sm) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdk::tb_kernel<T, K, V, REACT, MODE>, 32, 0) !=
+            cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+  }
+  const int64_t ctas = (int64_t)s->num_sms * per_sm;
+  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, K, ctas);
   const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
   const int64_t grid = std::min<int64_t>(tasks, ctas);
   rdk::tb_kernel<T, K, V, REACT, MODE><<<(unsigned)grid, 32, 0, s->stream>>>(a);
   return cudaGetLastError();
 }
 
+// Level-parallel variant for small (L2-resident) grids: CTAs of K warps.
+template <typename T, int K, bool REACT, int MODE>
+cudaError_t launch_lp_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_hi) {
+  constexpr int V = vec_of<T>();
+  using G = rdk::StripGeom<K, V>;
+  rdk::TBArgs<T> a;
+  fill_args<T>(s, a, in, out, out_lo, out_hi, K);
+  a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
+  static int per_sm = 0;
+  if (!per_sm) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdk::lp_kernel<T, K, V, REACT, MODE>, 32 * K, 0) !=
+            cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+  }
+  const int64_t ctas = (int64_t)s->num_sms * per_sm;
+  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, K + (K + 1) / 2, ctas);  // task ~ hb + 3K rows
+  const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
+  rdk::lp_kernel<T, K, V, REACT, MODE><<<(unsigned)std::min<int64_t>(tasks, ctas), 32 * K, 0, s->stream>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, bool REACT, int MODE>
 cudaError_t launch_tb_k(rd_sim* s, int k, int in, int out, int32_t lo, int32_t hi) {
+  if (s->use_lp && k <= 4) {
+    switch (k) {
+      case 1: return launch_lp_t<T, 1, REACT, MODE>(s, in, out, lo, hi);
+      case 2: return launch_lp_t<T, 2, REACT, MODE>(s, in, out, lo, hi);
+      case 3: return launch_lp_t<T, 3, REACT, MODE>(s, in, out, lo, hi);
+      case 4: return launch_lp_t<T, 4, REACT, MODE>(s, in, out, lo, hi);
+    }
+  }
   switch (k) {
     case 1: return launch_tb_t<T, 1, REACT, MODE>(s, in, out, lo, hi);
     case 2: return launch_tb_t<T, 2, REACT, MODE>(s, in, out, lo, hi);
@@ -343,6 +384,113 @@ int launch_tb(rd_sim* s, int k) {
   s->st.launches++;
   s->st.step_launches++;
   s->st.cell_updates += s->B * s->H * s->W * (int64_t)k;
+  return RD_OK;
+}
+
+// a8: shared memory per CTA of cr_kernel with cs CTAs per cluster.
+size_t cr_smem_bytes(const rd_sim* s, int cs) {
+  const int64_t V = 16 / (int64_t)s->esz;
+  const int64_t rows = (s->H + cs - 1) / cs, w4 = (s->W + V - 1) / V;
+  return (size_t)((rows + 2) * (w4 + 2) * V * 3 + rows * w4 * V * 2) * s->esz;
+}
+
+template <typename T, bool REACT, int MODE>
+cudaError_t launch_cr_t(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
+  static int nt_env = getenv("RD_CR_THREADS") ? atoi(getenv("RD_CR_THREADS")) : 0;
+  const int nt = nt_env == 512 || nt_env == 768 || nt_env == 1024 ? nt_env : rdk::cr_threads<T>();
+  auto fn = nt == 512 ? rdk::cr_kernel<T, REACT, MODE, 512>
+                      : (nt == 768 ? rdk::cr_kernel<T, REACT, MODE, 768> : rdk::cr_kernel<T, REACT, MODE, 1024>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)cs, (unsigned)s->B, 1);
+  cfg.blockDim = dim3((unsigned)nt, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (query) return cudaOccupancyMaxActiveClusters(clusters, fn, &cfg);
+  rdk::CrArgs<T> ca;
+  fill_args<T>(s, ca.a, s->cur, s->cur, 0, (int32_t)s->H, (int)n);
+  ca.a.n_strips = 0;
+  ca.a.hb = 0;
+  ca.cs = cs;
+  ca.n = (int32_t)n;
+  return cudaLaunchKernelEx(&cfg, fn, ca);
+}
+
+template <typename T>
+cudaError_t launch_cr_mode(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
+  if (s->g.flags & RD_REACTION_OFF) return launch_cr_t<T, false, rdk::MODE_PRECISE>(s, n, smem, cs, query, clusters);
+  if (sizeof(T) == 4 && s->fast_mode == rdk::MODE_FOLD_DIV4)
+    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4>(s, n, smem, cs, query, clusters);
+  return launch_cr_t<T, true, rdk::MODE_FOLD>(s, n, smem, cs, query, clusters);
+}
+
+cudaError_t cr_dispatch(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
+  return s->esz == 4 ? launch_cr_mode<float>(s, n, smem, cs, query, clusters)
+                     : launch_cr_mode<double>(s, n, smem, cs, query, clusters);
+}
+
+// Decide at create whether small instances run cluster-resident: the largest
+// cluster (16, 8, 4, 2 CTAs) whose per-CTA band fits in shared memory, used
+// when every instance's cluster is co-resident in one wave (larger batches
+// saturate the chip with tb_kernel). Fast modes only (precise replays and
+// checkpoint-less handles use tb_kernel), single-GPU handles only.
+void choose_cr(rd_sim* s, bool forced) {
+  s->use_cr = false;
+  if (s->slab || s->fast_mode == rdk::MODE_PRECISE) return;
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return;
+  const int64_t V = 16 / (int64_t)s->esz;
+  if ((s->W + V - 1) / V > 512) return;  // a thread per column vector (smallest block size)
+  for (int cs : {16, 8, 4, 2}) {
+    if (s->H < 2 * cs) continue;
+    const size_t smem = cr_smem_bytes(s, cs);
+    if (smem + 64 > (size_t)optin) continue;  // + the kernel's static mbarriers
+    int clusters = 0;
+    if (cr_dispatch(s, 0, smem, cs, true, &clusters) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (clusters < 1 || (!forced && clusters < s->B)) continue;
+    s->use_cr = true;
+    s->cr_cs = cs;
+    s->cr_smem = smem;
+    return;
+  }
+}
+
+// One cluster-resident launch of n steps, then the global mirrors.
+int launch_cr(rd_sim* s, int64_t n) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (s->profiling) {
+    if (s->ev_used == s->ev_pool.size()) {
+      cudaEvent_t a, b;
+      RD_CUDA(s, cudaEventCreate(&a));
+      RD_CUDA(s, cudaEventCreate(&b));
+      s->ev_pool.push_back({a, b});
+    }
+    e0 = s->ev_pool[s->ev_used].first;
+    e1 = s->ev_pool[s->ev_used].second;
+    ++s->ev_used;
+    RD_CUDA(s, cudaEventRecord(e0, s->stream));
+  }
+  cudaError_t e = cr_dispatch(s, n, s->cr_smem, s->cr_cs, false, nullptr);
+  if (e != cudaSuccess) return set_err(s, RD_ECUDA, "cr_kernel launch: %s", cudaGetErrorString(e));
+  if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
+  if (int rc = launch_mirror(s, s->u[s->cur], s->v[s->cur], nullptr, 0, (int32_t)s->H)) return rc;
+  s->st.launches++;
+  s->st.step_launches++;
+  s->st.cell_updates += s->B * s->H * s->W * n;
   return RD_OK;
 }
 
@@ -459,6 +607,11 @@ bool probe_due(const rd_sim* s, int64_t step) {
 // small-grid run costs one graph launch per segment instead of two kernel
 // launches per block (the per-launch overhead dominates small batched grids).
 int run_blocks(rd_sim* s, int64_t next, int kmax) {
+  if (s->use_cr && !s->precise_mode && !(s->g.flags & RD_NO_CHECKPOINT) && next > s->step) {
+    if (int rc = launch_cr(s, next - s->step)) return rc;
+    s->step = next;
+    return RD_OK;
+  }
   const bool graph = !(s->g.flags & RD_NO_GRAPH) && !s->profiling && !s->slab && !s->precise_mode &&
                      !s->graphs_broken && next - s->step >= 2 * kmax;
   if (!graph) {
@@ -684,6 +837,17 @@ bool foldable(const rd_params& p) {
 // Arithmetic mode for the handle's parameter set(s): FOLD when every 1/dx^2
 // is a power of two, FOLD_DIV4 when additionally (fp32, reaction on) the
 // 4-op division is certified for every q; else PRECISE.
+// Stencil kernel choice: cr_kernel for small instances that fit one wave of
+// clusters, else tb_kernel. RD_KERNEL=tb|lp|cr forces one (tests,
+// measurements; cr still needs the instance to fit shared memory).
+void select_kernels(rd_sim* s) {
+  const char* e = getenv("RD_KERNEL");
+  const std::string want = e ? e : "auto";
+  s->use_lp = want == "lp";
+  s->use_cr = false;
+  if (want == "auto" || want == "cr") choose_cr(s, want == "cr");
+}
+
 int choose_mode(rd_sim* s) {
   std::vector<rd_params> sets = s->pinst.empty() ? std::vector<rd_params>{s->p} : s->pinst;
   bool fold = true;
@@ -777,6 +941,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   }
   if (int rc = alloc_planes(s)) return fail(rc);
   if (int rc = choose_mode(s)) return fail(rc);
+  select_kernels(s);
   // phi rows present in the host buffer: local [lo, hi)
   const int64_t lo = slab ? std::max<int64_t>(0, row0 - halo) - row0 : 0;
   const int64_t hi = slab ? std::min<int64_t>(Hg, row0 + s->H + halo) - row0 : s->H;
@@ -1114,7 +1279,9 @@ int rd_set_params(rd_sim* s, int32_t b, const rd_params* p) {
     s->pinst[(size_t)b] = *p;
   }
   drop_graphs(s);  // constants are baked into captured launches
-  return choose_mode(s);
+  if (int rc = choose_mode(s)) return rc;
+  select_kernels(s);  // the fast mode decides whether cr_kernel applies
+  return RD_OK;
 }
 
 int rd_paint_phi(rd_sim* s, int32_t b, const rd_rect* r, double value) {
@@ -1261,6 +1428,7 @@ int rd_get_stats(rd_sim* s, rd_stats* out) {
   out->timed_launches = s->acc_timed;
   out->tb_depth = s->K;
   out->arith_mode = (s->g.flags & RD_NO_CHECKPOINT) ? rdk::MODE_PRECISE : s->fast_mode;
+  out->kernel = (s->use_cr && !(s->g.flags & RD_NO_CHECKPOINT)) ? 2 : (s->use_lp ? 1 : 0);
   return RD_OK;
 }
 

@@ -70,12 +70,16 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4")
     ap.add_argument("--dtype", default="both")
     ap.add_argument("--tb", type=int, default=0)
+    ap.add_argument("--repeat", type=int, default=2, help="runs per config; the last is reported (the first "
+                    "warms clocks, caches and graph captures)")
     a = ap.parse_args()
     dts = {"f32": [np.float32], "f64": [np.float64], "both": [np.float32, np.float64]}[a.dtype]
     for n in map(int, a.configs.split(",")):
         for dt in dts:
             if n in (4, 5) and dt == np.float64:
                 continue
+            for _ in range(a.repeat - 1):
+                run(n, dt, a.tb)
             print(json.dumps(run(n, dt, a.tb)), flush=True)
 
 

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
-def test_and_gate_batched_truth_table(dtype):
+def test_and_gate_batched_truth_table(dtype, kernel):
     """configs[1]: 4 truth-table rows in one batched launch; fields and probe
     latches bitwise equal to the oracle; output fires only for 11
     (PAPER.md:280-285)."""
@@ -35,7 +35,7 @@ def test_and_gate_batched_truth_table(dtype):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
-def test_diode_batched(dtype):
+def test_diode_batched(dtype, kernel):
     """configs[2]: both directions in one batched launch; anode->cathode
     crosses, cathode->anode does not."""
     w = config(3, dtype=dtype)

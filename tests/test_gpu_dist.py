@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("G,halo", [(2, 1), (2, 4), (3, 4), (4, 8)])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
-def test_virtual_slabs_equal_single_grid(G, halo, dtype):
+def test_virtual_slabs_equal_single_grid(G, halo, dtype, kernel):
     H, W, steps = 203, 300, 37
     rects = obstacles(H, W, 6, seed=3)
 

@@ -36,7 +36,7 @@ def _noise_workload(H, W, dtype, steps, B=1, phi=None, n_discs=6, seed=1, mask=N
 # ------------------------------------------------------------- config 1
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
-def test_config1_bitwise(dtype):
+def test_config1_bitwise(dtype, kernel):
     """configs[0]: 128x128 centred disc, 1000 steps, fields bitwise equal to
     the oracle (fp64: max|du|,|dv| = 0 <= 1e-10)."""
     w = config(1, dtype=dtype)
@@ -63,7 +63,7 @@ def test_config1_fp32_vs_fp64_oracle_early():
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
 @pytest.mark.parametrize("H,W", [(3, 3), (37, 131), (130, 250), (64, 517), (301, 29)])
-def test_ragged_shapes_all_depths(dtype, H, W):
+def test_ragged_shapes_all_depths(dtype, H, W, kernel):
     """Ragged grids (W not a multiple of the vector width or strip, tiny and
     tall/narrow) spanning several strips and row blocks: every tb_depth 1..8
     equals the oracle bitwise from a noisy initial state with stimuli."""
@@ -77,7 +77,7 @@ def test_ragged_shapes_all_depths(dtype, H, W):
 
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
-def test_batched_equals_unbatched_and_oracle(dtype):
+def test_batched_equals_unbatched_and_oracle(dtype, kernel):
     """a8: a batch of 3 different instances (own phi, init and stimuli) equals
     each instance run alone and the oracle."""
     H, W = 90, 140
@@ -94,7 +94,7 @@ def test_batched_equals_unbatched_and_oracle(dtype):
 
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
-def test_step_splitting_and_events(dtype):
+def test_step_splitting_and_events(dtype, kernel):
     """rd_step(a); rd_step(b) == rd_step(a+b) with events at
     steps inside, at and across the split points."""
     H, W = 70, 90
@@ -161,7 +161,7 @@ def test_probes_latch_and_immediate(dtype):
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
 @pytest.mark.parametrize("tb", [1, 4, 8])
-def test_nonfinite_fault_matches_oracle(dtype, tb):
+def test_nonfinite_fault_matches_oracle(dtype, tb, kernel):
     """T5: uniform phi=0.2, noisy u,v, an unmasked u:=1 half-disc -> Euler
     diverges. rd_step returns RD_ENONFINITE, the handle stops at the oracle's
     failing step with the oracle's first (i, j) and identical fields."""
@@ -206,7 +206,7 @@ def test_write_fields_rejects_nonfinite():
 
 
 @pytest.mark.parametrize("tb", [1, 4])
-def test_fast_division_guard_replay(tb):
+def test_fast_division_guard_replay(tb, kernel):
     """Cells with C + q below 2^-60 in magnitude trip the fast-division guard:
     the rd_step is replayed precisely from its checkpoint (stats.replays) and
     the result equals the oracle bitwise (finite or at the first fault)."""
@@ -238,7 +238,7 @@ def test_fast_division_guard_replay(tb):
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
 @pytest.mark.parametrize("stride,tb", [(25, 4), (7, 4), (50, 1), (3, 8)])
-def test_timelapse_matches_oracle(dtype, stride, tb):
+def test_timelapse_matches_oracle(dtype, stride, tb, kernel):
     """f2: the fused timelapse max_u, recorded after
     every multiple of stride, equals the oracle's bitwise; splitting rd_step
     calls does not change it."""
@@ -290,10 +290,12 @@ def test_rest_init_and_spiral_seeding(dtype):
 
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
-def test_graph_replay_equals_direct_launches(dtype):
+def test_graph_replay_equals_direct_launches(dtype, monkeypatch):
     """CUDA-graph replay of rd_step segments (default) and direct launches
-    (RD_NO_GRAPH) give bitwise identical fields and probe latches."""
+    (RD_NO_GRAPH) give bitwise identical fields and probe latches (tb_kernel:
+    cr_kernel segments are single launches and are not captured)."""
     from rdinputs import config
+    monkeypatch.setenv("RD_KERNEL", "tb")
     w = config(2, dtype=dtype, steps=1500)
     Ug, Vg, Fg, sg = gpu_run(w)
     Ud, Vd, Fd, sd = gpu_run(w, flags=rd.RD_NO_GRAPH)
