@@ -13,3 +13,7 @@ CMD2="python bench.py --timesteps 100 --steps 2 --warmup 3 --e2e-steps 0 --no-cp
 $CMD2 > gpurun_out/plain_full.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:tb_kernel -s 20 -c 1 -o gpurun_out/prof_full $CMD2 > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
+CMD3="python scripts/bench_configs.py --configs 2 --dtype f32 --repeat 1"
+$CMD3 > gpurun_out/plain_cr.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:cr_kernel -s 20 -c 1 -o gpurun_out/prof_cr $CMD3 > gpurun_out/ncu_cr.log 2>&1
+echo "cr rc=$?"

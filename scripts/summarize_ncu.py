@@ -79,6 +79,8 @@ def main():
     ap.add_argument("--round", default="r01")
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches.csv"))
     ap.add_argument("--full", default=os.path.join(ROOT, "gpurun_out", "prof_full.ncu-rep"))
+    ap.add_argument("--cr", default=os.path.join(ROOT, "gpurun_out", "prof_cr.ncu-rep"),
+                    help="--set full capture of cr_kernel (config 2)")
     ap.add_argument("--cmd", default="")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
@@ -99,6 +101,11 @@ def main():
                   open(os.path.join(PROF, f"traffic_{a.round}.json"), "w"), indent=1)
         for k, v in F.items():
             print(k, v)
+    if os.path.exists(a.cr):
+        F = full(a.cr)
+        F["source"] = f"ncu --set full capture ({os.path.basename(a.cr)}), config 2 fp32"
+        json.dump(F, open(os.path.join(PROF, f"{a.round}_cr_kernel_full.json"), "w"), indent=1)
+        print("cr_kernel:", {k: F[k] for k in ("gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in F})
 
 
 if __name__ == "__main__":
