@@ -44,6 +44,24 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+# ALU roofline of the temporally blocked kernel: the canonical
+# tree is 13 add/sub + 9 mul + 1 div = 23 fp32 operations per cell-update
+# (R-8); the FP32 pipe peak is 148 SMs x 128 lanes x clocks.max.sm, one
+# operation per lane per cycle (B200_PROFILING.md: 148 SMs, 1965 MHz).
+OPS_PER_CELL = 23
+FP32_LANES = 148 * 128
+
+
+def alu_peak_tops():
+    mhz, src = 1965.0, "B200_PROFILING.md clocks.max.sm"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mhz, src = float(json.load(fh)["sm_max_mhz"]), "MEASURED_PEAKS.json sm_max_mhz"
+    except Exception:
+        pass
+    return FP32_LANES * mhz * 1e6 / 1e12, f"derived: 148 SMs x 128 FP32 lanes x {mhz:.0f} MHz ({src})"
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -192,13 +210,21 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-                "kernel": f"tb_kernel<float,K={st['tb_depth']}>", "peak_source": hbm_src,
-                "algorithmic_bytes_per_cell_update": bpc,
+    # temporal blocking moves the kernel off the HBM roof (DRAM bytes per
+    # launch ~ one step's, ncu) onto the FP32 pipe: report the ALU bound, with
+    # the one-step HBM view beside it
+    alu, alu_src = alu_peak_tops()
+    ops = OPS_PER_CELL * st["cell_updates"] / (kms / 1e3) / 1e12 if kms > 0 else None
+    roofline = {"bound": "alu", "achieved": ops, "peak": alu, "unit": "TFLOP/s",
+                "frac": (ops / alu) if ops else None, "traffic": traffic,
+                "kernel": f"tb_kernel<float,K={st['tb_depth']}>", "peak_source": alu_src,
+                "algorithmic_ops_per_cell_update": OPS_PER_CELL,
+                "ops": "fp32 add/sub/mul/div of the canonical Eq.-1 tree (13 + 9 + 1), R-8",
                 "cell_updates_per_launch": st["cell_updates"] / k_launches,
                 "avg_launch_ms": kms / k_launches, "kernel_share_of_step": kms / ms if ms else None,
-                "one_step_roofline_gcells": hbm / bpc}
+                "hbm_view": {"achieved": achieved, "peak": hbm, "unit": "GB/s",
+                             "frac": (achieved / hbm) if achieved else None, "peak_source": hbm_src,
+                             "algorithmic_bytes_per_cell_update": bpc, "one_step_roofline_gcells": hbm / bpc}}
 
     # e2e through the public C ABI with pinned host buffers (1 GPU only)
     e2e = None
