@@ -4,6 +4,8 @@
 // phi, checkpoint), the pending stimulus queue, latched probes and the fault
 // word, and cuts every rd_step(n) into temporally blocked launches at event
 // and probe steps.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,6 +44,10 @@ struct LatchedProbe {
 }  // namespace
 
 struct rd_sim {
+  // tb_kernel input maps, one per input buffer (u[i], v[i], phi at a constant
+  // stride; see alloc_planes)
+  CUtensorMap tmap[2];
+  void* arena = nullptr;  // the plane allocation (u, v, phi, checkpoint)
   rd_grid g{};
   rd_params p{};
   size_t esz = 4;
@@ -259,6 +265,9 @@ void fill_args(rd_sim* s, rdk::TBArgs<T>& a, int in, int out, int32_t out_lo, in
   } else {
     for (int64_t b = 0; b < s->B; ++b) a.k[b] = make_consts<T>(s->pinst[b]);
   }
+  a.tmap = s->tmap[in];
+  a.tm_col0 = (int32_t)s->col_off;
+  a.tm_row0 = (int32_t)s->row_off;
   a.fault_key = s->d_fault;
   a.precise_flag = s->d_precise;
   a.tl = (s->tl_stride > 0 && (s->step + K) % s->tl_stride == 0) ? origin<T>(s, s->tl) : nullptr;
@@ -766,22 +775,60 @@ int restore_checkpoint(rd_sim* s) {
   return reset_fault(s);
 }
 
+// One allocation of seven plane blocks (a block = the plane of all B
+// instances): u0 | ck_u | u1 | v0 | v1 | ck_v | phi. Then u0, v0, phi sit at
+// a stride of 3 blocks and u1, v1, phi at a stride of 2, so one tensor map per
+// input buffer (dims col, row, instance, plane) lands a row's u, v and phi
+// segments with one TMA (tb_kernel). The checkpoint fills the two gaps.
 int alloc_planes(rd_sim* s) {
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
-  void** ps[5] = {&s->u[0], &s->u[1], &s->v[0], &s->v[1], &s->phi};
-  for (void** p : ps) {
-    RD_CUDA(s, cudaMalloc(p, bytes));
-    RD_CUDA(s, cudaMemsetAsync(*p, 0, bytes, s->stream));
-  }
+  RD_CUDA(s, cudaMalloc(&s->arena, 7 * bytes));
+  RD_CUDA(s, cudaMemsetAsync(s->arena, 0, 7 * bytes, s->stream));
+  char* base = static_cast<char*>(s->arena);
+  s->u[0] = base;
+  s->u[1] = base + 2 * bytes;
+  s->v[0] = base + 3 * bytes;
+  s->v[1] = base + 4 * bytes;
+  s->phi = base + 6 * bytes;
   if (!(s->g.flags & RD_NO_CHECKPOINT)) {
-    RD_CUDA(s, cudaMalloc(&s->ck_u, bytes));
-    RD_CUDA(s, cudaMalloc(&s->ck_v, bytes));
+    s->ck_u = base + bytes;
+    s->ck_v = base + 5 * bytes;
   }
   RD_CUDA(s, cudaMalloc(&s->d_fault, 2 * sizeof(unsigned long long)));
   s->d_precise = reinterpret_cast<int*>(s->d_fault + 1);
   RD_CUDA(s, cudaMalloc(&s->d_flag, sizeof(int)));
   RD_CUDA(s, cudaMalloc(&s->d_scratch, 64));
   return reset_fault(s);
+}
+
+// The tensor maps of tb_kernel's input rows (driver entry point through the
+// runtime: no libcuda link). Box = one row segment of 32*V columns of the
+// three planes; coordinates are relative to the plane's allocation start.
+int encode_tmaps(rd_sim* s) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return set_err(s, RD_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t block = (cuuint64_t)s->B * s->plane_stride * s->esz;
+  const cuuint32_t seg = (cuuint32_t)(32 * (16 / s->esz));
+  for (int i = 0; i < 2; ++i) {
+    const cuuint64_t dims[4] = {(cuuint64_t)s->pitch, (cuuint64_t)s->rows_alloc, (cuuint64_t)s->B, 3};
+    const cuuint64_t strides[3] = {(cuuint64_t)(s->pitch * s->esz), (cuuint64_t)(s->plane_stride * s->esz),
+                                   (i == 0 ? 3 : 2) * block};
+    const cuuint32_t box[4] = {seg, 1, 1, 3};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(&s->tmap[i], s->esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                        4, s->u[i], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(s, RD_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
+  return RD_OK;
 }
 
 int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
@@ -940,6 +987,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
     if (s->num_sms < 1) s->num_sms = 148;
   }
   if (int rc = alloc_planes(s)) return fail(rc);
+  if (int rc = encode_tmaps(s)) return fail(rc);
   if (int rc = choose_mode(s)) return fail(rc);
   select_kernels(s);
   // phi rows present in the host buffer: local [lo, hi)
@@ -1040,9 +1088,8 @@ int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi
 int rd_destroy(rd_sim* s) {
   if (!s) return RD_OK;
   if (s->stream) cudaStreamSynchronize(s->stream);
-  void* ps[] = {s->u[0],  s->u[1],       s->v[0],  s->v[1],   s->phi,       s->ck_u,     s->ck_v,
-                s->tl,    s->ck_tl,      s->d_probes, s->d_first, s->d_first_ck, s->d_fault, s->d_flag,
-                s->d_scratch};
+  void* ps[] = {s->arena, s->tl,       s->ck_tl,     s->d_probes, s->d_first,
+                s->d_first_ck, s->d_fault, s->d_flag, s->d_scratch};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& e : s->ev_pool) {
