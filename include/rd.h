@@ -132,7 +132,8 @@ typedef struct {
   int32_t tb_depth;        /* temporal-blocking depth in use */
   int32_t pad;
   int64_t replays;         /* rd_step calls replayed from the checkpoint (fault or fast-division guard) */
-  int32_t arith_mode;      /* 0 precise (canonical ops), 2 exact rewrites, 3 exact rewrites + certified 4-op fp32 division */
+  int32_t arith_mode;      /* 0 precise (canonical ops), 2 exact rewrites, 3 exact rewrites + certified 4-op fp32 division,
+                              4 as 3 without the min|C+q| guard (fp32 q >= 2^-35) */
   int32_t kernel;          /* stencil kernel of the fast path: 0 tb_kernel (temporal-blocked streaming),
                               1 lp_kernel (level-parallel), 2 cr_kernel (cluster-resident, a8) */
 } rd_stats;

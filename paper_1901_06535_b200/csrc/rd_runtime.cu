@@ -374,6 +374,8 @@ int launch_tb(rd_sim* s, int k) {
       e = launch_tb_k<float, false, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
     else if (precise)
       e = launch_tb_k<float, true, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
+    else if (s->fast_mode == rdk::MODE_FOLD_DIV4_NG)
+      e = launch_tb_k<float, true, rdk::MODE_FOLD_DIV4_NG>(s, k, in, out, lo, hi);
     else if (s->fast_mode == rdk::MODE_FOLD_DIV4)
       e = launch_tb_k<float, true, rdk::MODE_FOLD_DIV4>(s, k, in, out, lo, hi);
     else
@@ -437,6 +439,8 @@ cudaError_t launch_cr_t(rd_sim* s, int64_t n, size_t smem, int cs, bool query, i
 template <typename T>
 cudaError_t launch_cr_mode(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
   if (s->g.flags & RD_REACTION_OFF) return launch_cr_t<T, false, rdk::MODE_PRECISE>(s, n, smem, cs, query, clusters);
+  if (sizeof(T) == 4 && s->fast_mode == rdk::MODE_FOLD_DIV4_NG)
+    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4_NG>(s, n, smem, cs, query, clusters);
   if (sizeof(T) == 4 && s->fast_mode == rdk::MODE_FOLD_DIV4)
     return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4>(s, n, smem, cs, query, clusters);
   return launch_cr_t<T, true, rdk::MODE_FOLD>(s, n, smem, cs, query, clusters);
@@ -908,6 +912,11 @@ int choose_mode(rd_sim* s) {
       all = all && ok;
     }
     if (all) s->fast_mode = rdk::MODE_FOLD_DIV4;
+    // q >= 2^-35 in fp32: |C+q| < 2^-60 only at C+q == 0, which the
+    // non-finite check catches (rd_kernels.cuh Div<.., MODE_FOLD_DIV4_NG>)
+    bool big_q = true;
+    for (const auto& p : sets) big_q = big_q && (float)p.q >= 0x1p-35f;
+    if (all && big_q) s->fast_mode = rdk::MODE_FOLD_DIV4_NG;
   }
   return RD_OK;
 }

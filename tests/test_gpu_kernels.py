@@ -30,13 +30,14 @@ def test_fast_division_exhaustive(divcheck, q):
 
 def test_certified_four_op_division_selected_for_table1_q():
     """For Table-1 q the 4-op division is certified exhaustively at rd_create
-    and selected (arith_mode 3); a q where it is not exact keeps the 6-op
-    sequence (arith_mode 2); results are bitwise the oracle's either way."""
+    and selected without the min|C+q| guard (arith_mode 4: q >= 2^-35); a q
+    where it is not exact keeps the 6-op sequence (arith_mode 2); results are
+    bitwise the oracle's either way."""
     import numpy as np
     import oracle
     import paper_1901_06535_b200 as rd
     from rdinputs import config
-    for q, mode in ((0.002, 3), (0.1, 2)):
+    for q, mode in ((0.002, 4), (0.1, 2)):
         p = rd.rd_params_default()
         p.q = q
         w = config(1, dtype=np.float32, steps=200)

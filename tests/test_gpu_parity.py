@@ -206,21 +206,36 @@ def test_write_fields_rejects_nonfinite():
 
 
 @pytest.mark.parametrize("tb", [1, 4])
-def test_fast_division_guard_replay(tb, kernel):
-    """Cells with C + q below 2^-60 in magnitude trip the fast-division guard:
-    the rd_step is replayed precisely from its checkpoint (stats.replays) and
-    the result equals the oracle bitwise (finite or at the first fault)."""
+@pytest.mark.parametrize("qv,mode", [(0.002, 4), (2.0 ** -40, None)], ids=["q=0.002", "q=2^-40"])
+def test_fast_division_guard_replay(tb, kernel, qv, mode):
+    """Cells where the fast division is not certified make the rd_step replay
+    precisely from its checkpoint (stats.replays); the result equals the
+    oracle bitwise (finite or at the first fault).
+    q = 0.002 (guard-free mode 4): C = -q gives C + q == 0, so the fast
+    sequence yields NaN and the non-finite check triggers the replay (C one
+    ulp above -q gives C + q = 2^-32, inside the certified range).
+    q = 2^-40 (guarded modes): C = -q + ulp gives 0 < C + q = 2^-63 < 2^-60,
+    which the min|C+q| guard catches."""
     H, W = 24, 40
     dtype = np.float32
-    q = np.float32(0.002)
+    q = np.float32(qv)
     u0 = noise_plane(H, W, 0, seed=9, dtype=dtype)
     v0 = noise_plane(H, W, 1, seed=9, dtype=dtype)
-    # C = -q + tiny: b = C + q in (0, 2^-60); C exactly -q: b = 0
-    u0[5, 7] = np.nextafter(-q, np.float32(0))
-    u0[12, 30] = -q
+    if mode == 4:
+        u0[5, 7] = np.nextafter(-q, np.float32(0))
+        u0[12, 30] = -q
+    else:
+        u0[5, 7] = np.nextafter(-q, np.float32(0))
+        assert 0 < np.float32(u0[5, 7] + q) < np.float32(2.0 ** -60)
     phi = np.full((H, W), 0.054, dtype)
-    ref = oracle.run(u0, v0, phi, 6)
-    sim = rd.Sim(phi, dtype=dtype, tb_depth=tb)
+    ref = oracle.run(u0, v0, phi, 6, params=oracle.Params(q=float(q)))
+    p = rd.rd_params_default()
+    p.q = float(q)
+    sim = rd.Sim(phi, dtype=dtype, tb_depth=tb, params=p)
+    if mode is not None:
+        assert sim.stats()["arith_mode"] == mode
+    else:
+        assert sim.stats()["arith_mode"] in (2, 3)
     sim.write(0, u0, v0)
     try:
         sim.step(6)
