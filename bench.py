@@ -113,6 +113,26 @@ def dist_env():
     return world, rank, local
 
 
+def host_cores() -> int:
+    """Host cores this process may run on (the oracle's OpenMP threads)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    """Device-timed milliseconds -> max over ranks (all_reduce MAX)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ------------------------------------------------------------- our arm
 
 def run_ours(args):
@@ -122,10 +142,17 @@ def run_ours(args):
     from rdinputs import config
 
     world, rank, local = dist_env()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # RD_BENCH_BACKEND=gloo: functional check of this N > 1 path with
+        # several ranks on one GPU (host-staged halos; not a measurement)
+        backend = os.environ.get("RD_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dtype = np.dtype(np.float32)
     T = args.timesteps
     hbm, hbm_src = peaks()
@@ -160,7 +187,7 @@ def run_ours(args):
             slab.stimulate(shape, val, at)
         stepper = slab.step
         cells = slab.rows * W
-        u0 = v0 = None
+        u0, v0 = slab.read_owned(0)  # host copies of this rank's rows for the e2e leg
         workload = {"workload": f"configs[4] weak scaling: ({H})x{W} fp32 row slabs, 16 obstacles/GPU phi=0.2, "
                                 "masked half-discs, NCCL halo exchange", "grid": [H, W]}
     stream = torch.cuda.current_stream()
@@ -189,12 +216,7 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     st = rd.rd_get_stats(h)
     rd.rd_set_profiling(h, False)
-    ms_max = ms
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, world)
     total_updates = cells * world * T * args.steps
     value = total_updates / (ms_max / 1e3) / 1e9
 
@@ -226,28 +248,34 @@ def run_ours(args):
                              "frac": (achieved / hbm) if achieved else None, "peak_source": hbm_src,
                              "algorithmic_bytes_per_cell_update": bpc, "one_step_roofline_gcells": hbm / bpc}}
 
-    # e2e through the public C ABI with pinned host buffers (1 GPU only)
+    # e2e through the public API with pinned host buffers: every step writes
+    # this rank's u, v from the host, steps, and reads u, v back (N > 1: the
+    # owned rows of each slab; time = max over ranks)
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
-        pu = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
-        pv = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+    if args.e2e_steps > 0:
+        rows = u0.shape[0]
+        pu = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
+        pv = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
         pu[...] = u0
         pv[...] = v0
-        ou = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
-        ov = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
-        torch.cuda.synchronize()
+        ou = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
+        ov = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
+        barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.e2e_steps):
             rd.rd_write_fields(h, 0, pu, pv)
-            rd.rd_step(h, T)
+            stepper(T)
             rd.rd_read_fields(h, 0, ou, ov)
         b.record(stream)
-        torch.cuda.synchronize()
-        ems = a.elapsed_time(b)
-        e2e = {"value": cells * T * args.e2e_steps / (ems / 1e3) / 1e9, "unit": UNIT,
+        barrier()
+        ems = max_over_ranks(a.elapsed_time(b), world)
+        e2e = {"value": cells * world * T * args.e2e_steps / (ems / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 2 * cells * 4, "d2h_bytes_per_step": 2 * cells * 4,
-               "steps": args.e2e_steps, "api": "rd_write_fields(host pinned) + rd_step + rd_read_fields(host)"}
+               "steps": args.e2e_steps,
+               "api": ("rd_write_fields(host pinned) + rd_step + rd_read_fields(host)" if world == 1 else
+                       "per rank: rd_write_fields(host pinned, owned rows) + SlabSim.step (NCCL halos) + "
+                       "rd_read_fields(host); bytes per rank, time max over ranks")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -274,6 +302,7 @@ def cpu_baseline(u0, v0, phi, seconds: float):
     """The oracle, as it stands, on the host cores: a bounded sample of the same
     workload (the full grid for a few time steps, fp32 mode)."""
     import oracle
+    oracle.set_num_threads(host_cores())
     H, W = u0.shape
     t = time.perf_counter()
     oracle.run(u0, v0, phi, 1)
@@ -298,6 +327,7 @@ def run_reference(args):
         return
     import oracle
     from rdinputs import config
+    oracle.set_num_threads(host_cores())  # torchrun sets OMP_NUM_THREADS=1; rank 0 alone works here
     w = config(4)
     u, v = w.init_planes(0)
     phi = w.phi_plane(0).astype(np.float32)
