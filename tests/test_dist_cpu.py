@@ -119,3 +119,16 @@ def test_partition_covers_grid():
             assert rows[0][0] == 0 and sum(n for _, n in rows) == Hh
             for (a, n), (b, _) in zip(rows, rows[1:]):
                 assert a + n == b
+
+
+def test_sweep_shard_round_robin_covers_every_instance():
+    """SURVEY.md §8(e): batched instances are replicas, spread round-robin;
+    every instance runs on exactly one rank, loads differ by at most one."""
+    from paper_1901_06535_b200.sweep import shard
+    for n in (0, 1, 5, 8, 33):
+        for world in (1, 2, 3, 8):
+            parts = [shard(n, world, r) for r in range(world)]
+            flat = sorted(i for p in parts for i in p)
+            assert flat == list(range(n))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1

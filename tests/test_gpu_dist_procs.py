@@ -74,3 +74,45 @@ def test_two_process_slabs_equal_single_grid():
                      STEPS, events=_events())
     assert_bitwise(U, ref.u, "u")
     assert_bitwise(V, ref.v, "v")
+
+
+def _sweep_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1901_06535_b200.sweep import Instance, run_batch
+        from rdinputs import config
+        w = config(2)
+        inst = [Instance(w.phi_plane(b), w.events[b], w.probes[b]) for b in range(w.B)]
+        q.put((rank, run_batch(inst, w.steps, group=dist.group.WORLD)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_sweep_replicas_equal_one_process():
+    """SURVEY.md §8(e) replicas: the AND-gate batch (config 2) spread over two
+    ranks (round-robin, results all-gathered in instance order) gives the
+    same first-fire steps on every rank as one process running the whole
+    batch, and the paper's truth table 0001."""
+    from paper_1901_06535_b200.sweep import Instance, run_batch
+    from rdinputs import config
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    w = config(2)
+    one = run_batch([Instance(w.phi_plane(b), w.events[b], w.probes[b]) for b in range(w.B)], w.steps)
+    for _, fires in got:
+        assert fires == one
+    assert [f[0] >= 0 for f in one] == w.expect["fires"]
