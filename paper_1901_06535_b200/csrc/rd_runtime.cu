@@ -62,6 +62,13 @@ struct rd_sim {
   bool use_cr = false;  // a8 cluster-resident kernel (small instances, one wave)
   int cr_cs = 0;        // CTAs per cluster for cr_kernel
   size_t cr_smem = 0;   // its dynamic shared memory per CTA
+  bool cr_pal = false;  // cr_kernel with phi as palette indices
+  std::vector<std::vector<double>> pal;  // distinct phi values per instance (cr PAL layout)
+  bool pal_ok = true;     // every instance has <= 256
+  bool pal_dirty = true;  // device palette / index plane need a rebuild
+  uint8_t* d_idx = nullptr;
+  void* d_pal = nullptr;
+  int32_t* d_pal_n = nullptr;
   int64_t grow0 = 0, Hg = 0;
   bool slab = false;
   int top_edge = 1, bot_edge = 1;
@@ -399,18 +406,18 @@ int launch_tb(rd_sim* s, int k) {
 }
 
 // a8: shared memory per CTA of cr_kernel with cs CTAs per cluster.
-size_t cr_smem_bytes(const rd_sim* s, int cs) {
-  const int64_t V = 16 / (int64_t)s->esz;
+// a8: shared memory per CTA of cr_kernel with cs CTAs per cluster, phi as
+// values (pal = false) or as palette indices (pal = true).
+size_t cr_smem_bytes(const rd_sim* s, int cs, bool pal) {
+  const int V = 16 / (int)s->esz;
   const int64_t rows = (s->H + cs - 1) / cs, w4 = (s->W + V - 1) / V;
-  return (size_t)((rows + 2) * (w4 + 2) * V * 3 + rows * w4 * V * 2) * s->esz;
+  return (size_t)(rdk::cr_layout_elems(rows, w4, V, pal) * (int64_t)s->esz + (pal ? rows * w4 * V : 0));
 }
 
-template <typename T, bool REACT, int MODE>
+template <typename T, bool REACT, int MODE, bool PAL>
 cudaError_t launch_cr_t(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
-  static int nt_env = getenv("RD_CR_THREADS") ? atoi(getenv("RD_CR_THREADS")) : 0;
-  const int nt = nt_env == 512 || nt_env == 768 || nt_env == 1024 ? nt_env : rdk::cr_threads<T>();
-  auto fn = nt == 512 ? rdk::cr_kernel<T, REACT, MODE, 512>
-                      : (nt == 768 ? rdk::cr_kernel<T, REACT, MODE, 768> : rdk::cr_kernel<T, REACT, MODE, 1024>);
+  constexpr int nt = rdk::cr_threads<T>();
+  auto fn = rdk::cr_kernel<T, REACT, MODE, nt, PAL>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
@@ -431,31 +438,54 @@ cudaError_t launch_cr_t(rd_sim* s, int64_t n, size_t smem, int cs, bool query, i
   fill_args<T>(s, ca.a, s->cur, s->cur, 0, (int32_t)s->H, (int)n);
   ca.a.n_strips = 0;
   ca.a.hb = 0;
+  ca.idx = s->d_idx;
+  ca.pal = static_cast<const T*>(s->d_pal);
   ca.cs = cs;
   ca.n = (int32_t)n;
   return cudaLaunchKernelEx(&cfg, fn, ca);
 }
 
-template <typename T>
+template <typename T, bool PAL>
 cudaError_t launch_cr_mode(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
-  if (s->g.flags & RD_REACTION_OFF) return launch_cr_t<T, false, rdk::MODE_PRECISE>(s, n, smem, cs, query, clusters);
+  if (s->g.flags & RD_REACTION_OFF)
+    return launch_cr_t<T, false, rdk::MODE_PRECISE, PAL>(s, n, smem, cs, query, clusters);
   if (sizeof(T) == 4 && s->fast_mode == rdk::MODE_FOLD_DIV4_NG)
-    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4_NG>(s, n, smem, cs, query, clusters);
+    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4_NG, PAL>(s, n, smem, cs, query, clusters);
   if (sizeof(T) == 4 && s->fast_mode == rdk::MODE_FOLD_DIV4)
-    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4>(s, n, smem, cs, query, clusters);
-  return launch_cr_t<T, true, rdk::MODE_FOLD>(s, n, smem, cs, query, clusters);
+    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4, PAL>(s, n, smem, cs, query, clusters);
+  return launch_cr_t<T, true, rdk::MODE_FOLD, PAL>(s, n, smem, cs, query, clusters);
 }
 
-cudaError_t cr_dispatch(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
-  return s->esz == 4 ? launch_cr_mode<float>(s, n, smem, cs, query, clusters)
-                     : launch_cr_mode<double>(s, n, smem, cs, query, clusters);
+cudaError_t cr_dispatch(rd_sim* s, bool pal, int64_t n, size_t smem, int cs, bool query, int* clusters) {
+  if (s->esz == 4)
+    return pal ? launch_cr_mode<float, true>(s, n, smem, cs, query, clusters)
+               : launch_cr_mode<float, false>(s, n, smem, cs, query, clusters);
+  return pal ? launch_cr_mode<double, true>(s, n, smem, cs, query, clusters)
+             : launch_cr_mode<double, false>(s, n, smem, cs, query, clusters);
 }
 
-// Decide at create whether small instances run cluster-resident: the largest
-// cluster (16, 8, 4, 2 CTAs) whose per-CTA band fits in shared memory, used
-// when every instance's cluster is co-resident in one wave (larger batches
-// saturate the chip with tb_kernel). Fast modes only (precise replays and
-// checkpoint-less handles use tb_kernel), single-GPU handles only.
+// Per-step time models of the two small-grid paths, fitted to configs 1-3 on
+// B200 (scripts/bench_configs.py): cr_kernel costs a
+// barrier-and-exchange constant plus its band's cells on one SM; tb_kernel a
+// pipeline-latency floor plus the whole batch spread over the chip. fp64 cr
+// bands are ALU-latency bound (DFMA chains), so large fp64 batches of a few
+// instances stay on tb_kernel, which uses every SM.
+bool cr_beats_tb(const rd_sim* s, int cs) {
+  const bool f32 = s->esz == 4;
+  const double band = (double)((s->H + cs - 1) / cs) * (double)s->W;
+  const double total = (double)s->B * (double)s->H * (double)s->W;
+  const double t_cr = 0.3e-6 + band * (f32 ? 0.29e-9 : 0.64e-9);
+  const double t_tb = (f32 ? 2.9e-6 : 3.5e-6) + total * (f32 ? 1.9e-12 : 4.7e-12);
+  return t_cr < t_tb;
+}
+
+// Decide whether small instances run cluster-resident: the largest cluster
+// (16, 8, 4, 2 CTAs) whose per-CTA band fits in shared memory -- with phi as
+// values, else as palette indices when every instance's phi has <= 256
+// distinct values -- used when every instance's cluster is co-resident in
+// one wave (larger batches saturate the chip with tb_kernel). Fast modes only
+// (precise replays and checkpoint-less handles use tb_kernel), single-GPU
+// handles only. Re-evaluated when the parameters or the palettes change.
 void choose_cr(rd_sim* s, bool forced) {
   s->use_cr = false;
   if (s->slab || s->fast_mode == rdk::MODE_PRECISE) return;
@@ -467,19 +497,81 @@ void choose_cr(rd_sim* s, bool forced) {
   if ((s->W + V - 1) / V > 512) return;  // a thread per column vector (smallest block size)
   for (int cs : {16, 8, 4, 2}) {
     if (s->H < 2 * cs) continue;
-    const size_t smem = cr_smem_bytes(s, cs);
-    if (smem + 64 > (size_t)optin) continue;  // + the kernel's static mbarriers
-    int clusters = 0;
-    if (cr_dispatch(s, 0, smem, cs, true, &clusters) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
+    for (bool pal : {false, true}) {
+      if (pal && !s->pal_ok) continue;
+      const size_t smem = cr_smem_bytes(s, cs, pal);
+      if (smem + 64 > (size_t)optin) continue;  // + the kernel's static mbarriers
+      int clusters = 0;
+      if (cr_dispatch(s, pal, 0, smem, cs, true, &clusters) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (clusters < 1 || (!forced && (clusters < s->B || !cr_beats_tb(s, cs)))) continue;
+      s->use_cr = true;
+      s->cr_cs = cs;
+      s->cr_smem = smem;
+      s->cr_pal = pal;
+      return;
     }
-    if (clusters < 1 || (!forced && clusters < s->B)) continue;
-    s->use_cr = true;
-    s->cr_cs = cs;
-    s->cr_smem = smem;
-    return;
   }
+}
+
+// PAL: upload the palettes and rebuild the per-cell index plane after phi
+// changed (create, rd_paint_phi).
+int sync_palette(rd_sim* s) {
+  if (!s->pal_dirty) return RD_OK;
+  const int64_t n = s->B * s->H * s->W;
+  if (!s->d_idx) {
+    RD_CUDA(s, cudaMalloc(&s->d_idx, (size_t)n));
+    RD_CUDA(s, cudaMalloc(&s->d_pal, (size_t)s->B * 256 * s->esz));
+    RD_CUDA(s, cudaMalloc(&s->d_pal_n, (size_t)s->B * sizeof(int32_t)));
+  }
+  std::vector<unsigned char> hp((size_t)s->B * 256 * s->esz, 0);
+  std::vector<int32_t> hn((size_t)s->B);
+  for (int64_t b = 0; b < s->B; ++b) {
+    hn[b] = (int32_t)s->pal[b].size();
+    for (size_t i = 0; i < s->pal[b].size(); ++i) {
+      if (s->esz == 4) {
+        const float f = (float)s->pal[b][i];
+        std::memcpy(&hp[((size_t)b * 256 + i) * 4], &f, 4);
+      } else {
+        std::memcpy(&hp[((size_t)b * 256 + i) * 8], &s->pal[b][i], 8);
+      }
+    }
+  }
+  RD_CUDA(s, cudaMemcpyAsync(s->d_pal, hp.data(), hp.size(), cudaMemcpyHostToDevice, s->stream));
+  RD_CUDA(s, cudaMemcpyAsync(s->d_pal_n, hn.data(), hn.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s->stream));
+  RD_CUDA(s, cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream));
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((s->H * s->W + 255) / 256, 256)), (unsigned)s->B);
+  if (s->esz == 4)
+    rdk::phi_index_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, s->phi), s->plane_stride, s->pitch,
+                                                               (int32_t)s->H, (int32_t)s->W, (const float*)s->d_pal,
+                                                               s->d_pal_n, s->d_idx, s->d_flag);
+  else
+    rdk::phi_index_kernel<double><<<grid, 256, 0, s->stream>>>(origin<double>(s, s->phi), s->plane_stride, s->pitch,
+                                                                (int32_t)s->H, (int32_t)s->W, (const double*)s->d_pal,
+                                                                s->d_pal_n, s->d_idx, s->d_flag);
+  RD_CUDA(s, cudaGetLastError());
+  s->st.launches++;
+  int miss = 0;
+  RD_CUDA(s, cudaMemcpyAsync(&miss, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  if (miss) return set_err(s, RD_ECUDA, "phi palette out of sync with the phi plane");
+  s->pal_dirty = false;
+  return RD_OK;
+}
+
+// Palette bookkeeping (PAL layout of cr_kernel): the distinct phi values of
+// each instance in the working precision, tracked on the host from the
+// uploaded map and rd_paint_phi; more than 256 disables the PAL layout.
+void palette_add(rd_sim* s, int64_t b, double value) {
+  const double v = s->esz == 4 ? (double)(float)value : value;
+  auto& p = s->pal[(size_t)b];
+  for (double x : p)
+    if (x == v) return;
+  p.push_back(v);
+  if (p.size() > 256) s->pal_ok = false;
+  s->pal_dirty = true;
 }
 
 // One cluster-resident launch of n steps, then the global mirrors.
@@ -497,7 +589,9 @@ int launch_cr(rd_sim* s, int64_t n) {
     ++s->ev_used;
     RD_CUDA(s, cudaEventRecord(e0, s->stream));
   }
-  cudaError_t e = cr_dispatch(s, n, s->cr_smem, s->cr_cs, false, nullptr);
+  if (s->cr_pal)
+    if (int rc = sync_palette(s)) return rc;
+  cudaError_t e = cr_dispatch(s, s->cr_pal, n, s->cr_smem, s->cr_cs, false, nullptr);
   if (e != cudaSuccess) return set_err(s, RD_ECUDA, "cr_kernel launch: %s", cudaGetErrorString(e));
   if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
   if (int rc = launch_mirror(s, s->u[s->cur], s->v[s->cur], nullptr, 0, (int32_t)s->H)) return rc;
@@ -620,7 +714,8 @@ bool probe_due(const rd_sim* s, int64_t step) {
 // small-grid run costs one graph launch per segment instead of two kernel
 // launches per block (the per-launch overhead dominates small batched grids).
 int run_blocks(rd_sim* s, int64_t next, int kmax) {
-  if (s->use_cr && !s->precise_mode && !(s->g.flags & RD_NO_CHECKPOINT) && next > s->step) {
+  if (s->use_cr && (!s->cr_pal || s->pal_ok) && !s->precise_mode && !(s->g.flags & RD_NO_CHECKPOINT) &&
+      next > s->step) {
     if (int rc = launch_cr(s, next - s->step)) return rc;
     s->step = next;
     return RD_OK;
@@ -998,7 +1093,6 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   if (int rc = alloc_planes(s)) return fail(rc);
   if (int rc = encode_tmaps(s)) return fail(rc);
   if (int rc = choose_mode(s)) return fail(rc);
-  select_kernels(s);
   // phi rows present in the host buffer: local [lo, hi)
   const int64_t lo = slab ? std::max<int64_t>(0, row0 - halo) - row0 : 0;
   const int64_t hi = slab ? std::min<int64_t>(Hg, row0 + s->H + halo) - row0 : s->H;
@@ -1018,6 +1112,33 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
     }
   }
   if (int rc = launch_mirror(s, s->phi, s->u[0], s->v[0], s->r_lo, s->r_hi)) return fail(rc);
+  // cr_kernel PAL layout: the distinct phi values of every instance (only
+  // instances small enough for cr_kernel are scanned)
+  s->pal.assign((size_t)s->B, {});
+  s->pal_ok = !slab && s->H * s->W <= (int64_t)1 << 20;
+  for (int64_t b = 0; b < s->B && s->pal_ok; ++b) {
+    if (!phi_host) {
+      palette_add(s, b, 0.0);
+      continue;
+    }
+    std::vector<double> vals((size_t)(s->H * s->W));
+    const char* src = (const char*)phi_host + (size_t)b * s->H * s->W * s->esz;
+    for (size_t i = 0; i < vals.size(); ++i) {
+      if (s->esz == 4) {
+        float f;
+        std::memcpy(&f, src + 4 * i, 4);
+        vals[i] = f;
+      } else {
+        std::memcpy(&vals[i], src + 8 * i, 8);
+      }
+    }
+    std::sort(vals.begin(), vals.end());
+    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+    if (vals.size() > 256) s->pal_ok = false;
+    else
+      for (double v : vals) palette_add(s, b, v);
+  }
+  select_kernels(s);
   if (cudaStreamSynchronize(s->stream) != cudaSuccess) {
     s->err = "stream sync failed";
     return fail(RD_ECUDA);
@@ -1097,8 +1218,8 @@ int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi
 int rd_destroy(rd_sim* s) {
   if (!s) return RD_OK;
   if (s->stream) cudaStreamSynchronize(s->stream);
-  void* ps[] = {s->arena, s->tl,       s->ck_tl,     s->d_probes, s->d_first,
-                s->d_first_ck, s->d_fault, s->d_flag, s->d_scratch};
+  void* ps[] = {s->arena,   s->tl,    s->ck_tl,  s->d_probes, s->d_first, s->d_first_ck,
+                s->d_fault, s->d_flag, s->d_scratch, s->d_idx, s->d_pal, s->d_pal_n};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& e : s->ev_pool) {
@@ -1355,6 +1476,7 @@ int rd_paint_phi(rd_sim* s, int32_t b, const rd_rect* r, double value) {
     const int32_t b0 = b < 0 ? 0 : b, nb = b < 0 ? (int32_t)s->B : 1;
     const unsigned grid = (unsigned)std::min<int64_t>(((hi - lo) * (x1 - x0) + 255) / 256, s->num_sms * 16);
     for (int32_t i = b0; i < b0 + nb; ++i) {
+      if (s->pal_ok && !s->pal.empty()) palette_add(s, i, value);
       if (s->esz == 4)
         rdk::paint_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, s->phi), s->plane_stride, s->pitch,
                                                               (int32_t)lo, (int32_t)hi, x0, x1, (float)value, i);

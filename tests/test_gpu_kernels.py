@@ -57,7 +57,9 @@ def test_certified_four_op_division_selected_for_table1_q():
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_cluster_resident_kernel_selection_and_parity(dtype, monkeypatch):
     """a8: instances that fit a cluster's shared memory run on cr_kernel by
-    default (rd_stats.kernel == 2) -- configs 1-3 in fp32, config 1 in fp64 --
+    default (rd_stats.kernel == 2) when its cost model predicts a gain --
+    configs 1-3 in fp32, configs 1-2 in fp64 (config 2 with phi as palette
+    indices) --
     bitwise equal to the oracle and to tb_kernel, over row splits with and
     without a ragged remainder (H % cs != 0), narrow W (< one block of
     threads) and a segment cut by a mid-run stimulus."""
@@ -67,7 +69,9 @@ def test_cluster_resident_kernel_selection_and_parity(dtype, monkeypatch):
     from rdinputs import config, noise_plane
     dt = np.float32 if dtype == "f32" else np.float64
     monkeypatch.delenv("RD_KERNEL", raising=False)
-    fits = {1: True, 2: dt == np.float32, 3: dt == np.float32}
+    # fp64 config 3: the cost model keeps it on tb_kernel (all SMs) -- forced
+    # cr is covered below
+    fits = {1: True, 2: True, 3: dt == np.float32}
     for n, want in fits.items():
         w = config(n, dtype=dt)
         sim = rd.Sim(np.stack([w.phi_plane(b).astype(dt) for b in range(w.B)]), dtype=dt)
@@ -94,3 +98,103 @@ def test_cluster_resident_kernel_selection_and_parity(dtype, monkeypatch):
             sim.close()
             assert np.array_equal(out[kern][0], ref.u), (H, W, kern)
             assert np.array_equal(out[kern][1], ref.v), (H, W, kern)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("H,W", [(4, 3), (5, 3), (33, 3), (4, 5), (17, 8), (6, 4), (64, 2048), (40, 1021)])
+def test_cluster_resident_edge_shapes(dtype, H, W, monkeypatch):
+    """cr_kernel at its shape limits: bands of one or two rows (H = 4, 5 with
+    2-CTA clusters), the narrowest grids the API accepts (W = 3: the ghost
+    column W inside the only vector), exact multiples of the vector width
+    (ghost column W in the pad vector) and wide rows (one thread per vector,
+    up to 512 vectors) -- bitwise equal to the oracle, with a mid-segment
+    event and uneven rd_step splits."""
+    import numpy as np
+    import oracle
+    import paper_1901_06535_b200 as rd
+    from rdinputs import noise_plane
+    dt = np.float32 if dtype == "f32" else np.float64
+    monkeypatch.setenv("RD_KERNEL", "cr")
+    u0 = noise_plane(H, W, 0, seed=11, dtype=dt)
+    v0 = noise_plane(H, W, 1, seed=11, dtype=dt)
+    phi = np.full((H, W), 0.054, dt)
+    phi[:, W // 2:] = 0.0975
+    ev = [({"kind": "disc", "cy2": H, "cx2": W, "r": 2}, 1.0, 0),
+          ({"kind": "rect", "y0": H - 1, "x0": 0, "y1": H, "x1": W}, 1.0, 13)]
+    ref = oracle.run(u0, v0, phi, 30, events=ev)
+    sim = rd.Sim(phi[None], dtype=dt)
+    vec = 16 // np.dtype(dt).itemsize
+    fits = (W + vec - 1) // vec <= 512
+    assert sim.stats()["kernel"] == (2 if fits else 0)
+    sim.write(0, u0, v0)
+    for s, val, at in ev:
+        sim.stimulate(s, val, at)
+    for n in (7, 6, 17):
+        sim.step(n)
+    u, v = sim.read(0)
+    sim.close()
+    assert np.array_equal(u, ref.u) and np.array_equal(v, ref.v)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_cluster_resident_palette_layout(dtype, monkeypatch):
+    """cr_kernel with phi as palette indices (the layout that fits fp64
+    configs 2/3): a device-painted handle (phi = 0 plus painted values, the
+    palette tracked from rd_paint_phi, repainted between rd_step calls) and
+    a config-3-sized diode batch are bitwise equal to the oracle; a phi map
+    with more than 256 distinct values per instance falls back to tb_kernel
+    and stays exact."""
+    import numpy as np
+    import oracle
+    import paper_1901_06535_b200 as rd
+    from rdinputs import config, noise_plane
+    dt = np.float32 if dtype == "f32" else np.float64
+    monkeypatch.setenv("RD_KERNEL", "cr")
+    H, W = 300, 400  # config-2 instances: fp64 fits only with the palette layout
+    sim = rd.Sim(None, shape=(1, H, W), dtype=dt)
+    sim.paint_phi(0.054)
+    sim.paint_phi(0.0975, (100, 200, 140, 380))
+    assert sim.stats()["kernel"] == 2
+    u0 = noise_plane(H, W, 0, seed=5, dtype=dt)
+    v0 = noise_plane(H, W, 1, seed=5, dtype=dt)
+    sim.write(0, u0, v0)
+    sim.stimulate({"kind": "disc", "cy2": H, "cx2": 200, "r": 6}, 1.0, 0)
+    sim.step(25)
+    sim.paint_phi(0.2, (10, 10, 30, 60))   # a third value mid-run
+    sim.step(15)
+    u, v = sim.read(0)
+    st = sim.stats()
+    sim.close()
+    phi = np.full((H, W), 0.054, dt)
+    phi[100:140, 200:380] = dt(0.0975)
+    r1 = oracle.run(u0, v0, phi, 25, events=[({"kind": "disc", "cy2": H, "cx2": 200, "r": 6}, 1.0, 0)])
+    phi2 = phi.copy()
+    phi2[10:30, 10:60] = dt(0.2)
+    r2 = oracle.run(r1.u, r1.v, phi2, 15, step0=25)
+    assert st["kernel"] == 2
+    assert np.array_equal(u, r2.u) and np.array_equal(v, r2.v)
+    # AND-gate batch at config-2 size in this dtype (palette layout in fp64)
+    w = config(2, dtype=dt, steps=300)
+    phis = np.stack([w.phi_plane(b).astype(dt) for b in range(w.B)])
+    s2 = rd.Sim(phis, dtype=dt)
+    assert s2.stats()["kernel"] == 2
+    for b in range(w.B):
+        for sh, val, at in w.events[b]:
+            s2.stimulate(sh, val, at, b=b)
+    s2.step(w.steps)
+    for b in range(w.B):
+        ub, vb = s2.read(b)
+        u0b, v0b = w.init_planes(b)
+        ref = oracle.run(u0b, v0b, w.phi_plane(b).astype(dt), w.steps, events=w.events[b])
+        assert np.array_equal(ub, ref.u) and np.array_equal(vb, ref.v), b
+    s2.close()
+    # > 256 distinct phi values: no palette; fp64 does not fit otherwise
+    rough = (0.05 + 0.01 * noise_plane(H, W, 0, seed=6, dtype=np.float64)).astype(dt)
+    s3 = rd.Sim(rough[None], dtype=dt)
+    assert s3.stats()["kernel"] == (2 if dt == np.float32 else 0)
+    s3.write(0, u0, v0)
+    s3.step(12)
+    u3, v3 = s3.read(0)
+    s3.close()
+    ref3 = oracle.run(u0, v0, rough, 12)
+    assert np.array_equal(u3, ref3.u) and np.array_equal(v3, ref3.v)
