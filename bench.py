@@ -113,6 +113,21 @@ def dist_env():
     return world, rank, local
 
 
+def config_dict(world: int, T: int, tb_depth: int) -> dict:
+    """The `config` of the JSON line -- the same for our arm and the
+    reference arm (BASELINE.json configs[3] at N = 1,
+    configs[4] weak scaling at N > 1)."""
+    if world == 1:
+        d = {"workload": "configs[3] c4_roofline: 16384x16384 fp32, phi=0.054, u,v~U[0,0.1) seed 1, "
+                         "64 half-discs r=8 seed 2, no-flux", "grid": [16384, 16384]}
+    else:
+        d = {"workload": f"configs[4] weak scaling: ({16384 * world})x16384 fp32 row slabs, 16 obstacles/GPU "
+                         "phi=0.2, masked half-discs, NCCL halo exchange", "grid": [16384 * world, 16384]}
+    return dict(d, time_steps_per_step=T, tb_depth=tb_depth,
+                l2="inputs larger than L2 (5 x 1 GiB planes per GPU); no flush needed",
+                parallelism=f"row slabs x{world}" if world > 1 else "single GPU")
+
+
 def host_cores() -> int:
     """Host cores this process may run on (the oracle's OpenMP threads)."""
     try:
@@ -172,8 +187,6 @@ def run_ours(args):
             sim.stimulate(shape, val, at)
         stepper = sim.step
         cells = H * W
-        workload = {"workload": "configs[3] c4_roofline: 16384x16384 fp32, phi=0.054, u,v~U[0,0.1) seed 1, "
-                                "64 half-discs r=8 seed 2, no-flux", "grid": [H, W]}
     else:
         w = config(5, H=16384 * world, W=16384, n_obstacles=16 * world)
         H, W = w.H, w.W
@@ -188,8 +201,6 @@ def run_ours(args):
         stepper = slab.step
         cells = slab.rows * W
         u0, v0 = slab.read_owned(0)  # host copies of this rank's rows for the e2e leg
-        workload = {"workload": f"configs[4] weak scaling: ({H})x{W} fp32 row slabs, 16 obstacles/GPU phi=0.2, "
-                                "masked half-discs, NCCL halo exchange", "grid": [H, W]}
     stream = torch.cuda.current_stream()
     rd.rd_set_stream(h, rd.stream_handle(stream))  # engine work on the stream the events are recorded on
 
@@ -286,9 +297,7 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(workload, time_steps_per_step=T, tb_depth=st["tb_depth"],
-                               l2="inputs larger than L2 (5 x 1 GiB planes per GPU); no flush needed",
-                               parallelism=f"row slabs x{world}" if world > 1 else "single GPU"),
+                "config": config_dict(world, T, st["tb_depth"]),
                 "frac_of_one_step_hbm_roofline": value / world / (hbm / bpc),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
@@ -320,35 +329,47 @@ def cpu_baseline(u0, v0, phi, seconds: float):
 
 def run_reference(args):
     """--impl reference: the oracle (this tier's reference arm) timed as it
-    stands on the host cores, on our arm's config/metric/unit. Each step is a
-    bounded sample: one time step of the full 16384^2 fp32 grid."""
+    stands on the host cores, on our arm's config/metric/unit. Each bench step
+    is a bounded sample of that workload: four time steps of a 16384 x 16384
+    grid (N = 1: the config-4 grid; N > 1: rank 0's slab of the config-5
+    weak-scaling grid, obstacles included) in one oracle call, after an
+    untimed step 0 that applies the stimuli, so the run ends within minutes.
+    Under torchrun rank 0 alone works; the other ranks exit without work."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     import oracle
     from rdinputs import config
     oracle.set_num_threads(host_cores())  # torchrun sets OMP_NUM_THREADS=1; rank 0 alone works here
-    w = config(4)
+    if world == 1:
+        w = config(4)
+        sample = "4 time steps of the full 16384x16384 config-4 grid per bench step (after step 0's stimuli)"
+    else:
+        w = config(5, H=16384, W=16384, n_obstacles=16)
+        sample = "4 time steps of one 16384x16384 config-5 slab (rank 0's share) per bench step (after step 0)"
     u, v = w.init_planes(0)
     phi = w.phi_plane(0).astype(np.float32)
-    n = 1
+    # untimed: step 0 with the stimuli (our arm stamps them before its timed
+    # region too), then the warm-up steps
+    r = oracle.run(u, v, phi, 1, events=w.events[0])
+    cu, cv, s0 = r.u, r.v, 1
+    n = 4  # time steps per bench step: one oracle call, amortising its marshalling
     for _ in range(args.warmup):
-        r = oracle.run(u, v, phi, n, events=w.events[0])
+        r = oracle.run(cu, cv, phi, n, step0=s0)
+        cu, cv, s0 = r.u, r.v, s0 + n
     t = time.perf_counter()
-    cu, cv = u, v
-    for s in range(args.steps):
-        r = oracle.run(cu, cv, phi, n, events=w.events[0], step0=s)
-        cu, cv = r.u, r.v
+    for _ in range(args.steps):
+        r = oracle.run(cu, cv, phi, n, step0=s0)
+        cu, cv, s0 = r.u, r.v, s0 + n
     el = time.perf_counter() - t
     value = w.H * w.W * n * args.steps / el / 1e9
-    cfg = {"workload": "configs[3] c4_roofline: 16384x16384 fp32 (oracle fp32 mode)", "grid": [w.H, w.W],
-           "time_steps_per_step": n}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(world, args.timesteps, args.tb or 4),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": f"{n} time step(s) of the full grid per bench step"},
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
