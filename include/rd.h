@@ -201,6 +201,28 @@ int rd_step(struct rd_sim* sim, int64_t n);
  *                      since the checkpoint must be replayed); clears both.
  *   rd_restore         return to the last checkpoint. */
 int rd_checkpoint(struct rd_sim* sim);
+
+/* Halo exchange overlapped with interior compute (slab
+ * handles, same fast kernels as rd_step_unchecked):
+ *   rd_step_begin   opens a block of k (1 <= k <= halo) steps: if the block is
+ *                   one plain launch (k <= the handle's depth, no stimulus due
+ *                   in [step, step+k), no probe or timelapse sample strictly
+ *                   inside) it launches the interior rows -- those at least k
+ *                   rows from any exchanged ghost row, which read owned rows
+ *                   only -- and sets *started = 1; otherwise *started = 0,
+ *                   nothing is launched, and the caller steps the block with
+ *                   rd_step_unchecked once the exchange has landed.
+ *   rd_step_finish  after the exchange of the block's input rows has landed
+ *                   (on the handle's stream): launches the edge bands, flips
+ *                   the buffers, refreshes the mirrors, advances the step and
+ *                   runs probes due at the block's end.
+ * The exchange reads rows [0, halo) and [rows-halo, rows) and writes the
+ * ghost rows of the input buffer; the interior launch reads neither range's
+ * ghosts and writes only the output buffer, so both may run concurrently.
+ * Errors: RD_EINVAL (not a slab handle, block already open / not open),
+ * RD_ERANGE (k), RD_ECUDA. */
+int rd_step_begin(struct rd_sim* sim, int64_t k, int32_t* started);
+int rd_step_finish(struct rd_sim* sim);
 int rd_step_unchecked(struct rd_sim* sim, int64_t n);
 int rd_read_flags(struct rd_sim* sim, int32_t* nonfinite, int32_t* inexact);
 int rd_restore(struct rd_sim* sim);

@@ -21,7 +21,7 @@ from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_C
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
-           "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
+           "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_step_begin", "rd_step_finish", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -129,6 +129,21 @@ def rd_checkpoint(h) -> None:
 
 def rd_step_unchecked(h, n: int) -> None:
     _check(load().rd_step_unchecked(h, int(n)), h)
+
+
+def rd_step_begin(h, k: int) -> bool:
+    """Open a slab block of k steps and launch its interior rows (they need
+    no ghost rows) so they overlap the halo exchange; False: the block is not
+    one plain launch -- step it with rd_step_unchecked after the exchange."""
+    started = C.c_int32(0)
+    _check(load().rd_step_begin(h, int(k), C.byref(started)), h)
+    return bool(started.value)
+
+
+def rd_step_finish(h) -> None:
+    """Close the block opened by rd_step_begin once the exchange has landed:
+    edge bands, buffer flip, mirrors, step, probes."""
+    _check(load().rd_step_finish(h), h)
 
 
 def rd_read_flags(h) -> tuple[bool, bool]:

@@ -68,6 +68,8 @@ SYMBOLS = [
     ("rd_step", C.c_int, [P, i64]),
     ("rd_checkpoint", C.c_int, [P]),
     ("rd_step_unchecked", C.c_int, [P, i64]),
+    ("rd_step_begin", C.c_int, [P, i64, C.POINTER(i32)]),
+    ("rd_step_finish", C.c_int, [P]),
     ("rd_read_flags", C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     ("rd_restore", C.c_int, [P]),
     ("rd_get_step", C.c_int64, [P]),

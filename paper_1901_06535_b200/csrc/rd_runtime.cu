@@ -89,6 +89,7 @@ struct rd_sim {
   int cur = 0;
   int64_t step = 0;
   int32_t ghost_valid = 0;  // slab: ghost rows still valid in the current buffers
+  int32_t pending_k = 0;    // rd_step_begin opened a block of this many steps
   int K = 4;
   std::vector<PendingEvent> events;
   std::vector<LatchedProbe> probes;
@@ -349,10 +350,10 @@ cudaError_t launch_tb_k(rd_sim* s, int k, int in, int out, int32_t lo, int32_t h
   return cudaErrorInvalidValue;
 }
 
-int launch_tb(rd_sim* s, int k) {
-  const int in = s->cur, out = s->cur ^ 1;
-  if (s->slab && k > s->ghost_valid)
-    return set_err(s, RD_ERANGE, "slab ghost rows exhausted (k=%d > %d valid rows)", k, s->ghost_valid);
+// One stencil launch of k steps from buffer `in` to `out` producing rows
+// [lo, hi) (no buffer flip, no mirror refresh): profiling events and the
+// arithmetic-mode dispatch.
+int launch_rows(rd_sim* s, int k, int in, int out, int32_t lo, int32_t hi) {
   const bool react = !(s->g.flags & RD_REACTION_OFF);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (s->profiling) {
@@ -367,11 +368,6 @@ int launch_tb(rd_sim* s, int k) {
     ++s->ev_used;
     RD_CUDA(s, cudaEventRecord(e0, s->stream));
   }
-  // rows to produce: owned rows, plus at interior slab edges the ghost rows
-  // that stay valid for later launches of this rd_step (ghost depth g - k)
-  const int32_t keep = s->slab ? s->ghost_valid - k : 0;
-  const int32_t lo = s->top_edge ? 0 : -keep;
-  const int32_t hi = (int32_t)s->H + (s->bot_edge ? 0 : keep);
   cudaError_t e;
   // the fast modes (exact rewrites + guarded fp32 division) unless this is a
   // precise replay or there is no checkpoint to replay from
@@ -396,13 +392,36 @@ int launch_tb(rd_sim* s, int k) {
   }
   if (e != cudaSuccess) return set_err(s, RD_ECUDA, "tb_kernel<k=%d> launch: %s", k, cudaGetErrorString(e));
   if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
-  s->cur = out;
-  s->ghost_valid -= k;
-  if (int rc = launch_mirror(s, s->u[out], s->v[out], nullptr, lo, hi)) return rc;
   s->st.launches++;
   s->st.step_launches++;
-  s->st.cell_updates += s->B * s->H * s->W * (int64_t)k;
+  s->st.cell_updates += s->B * (int64_t)(std::min<int32_t>(hi, (int32_t)s->H) - std::max<int32_t>(lo, 0)) * s->W * k;
   return RD_OK;
+}
+
+// Rows one k-step launch produces: owned rows, plus at interior slab edges
+// the ghost rows that stay valid for later launches of this rd_step (ghost
+// depth g - k).
+void block_rows(const rd_sim* s, int k, int32_t* lo, int32_t* hi) {
+  const int32_t keep = s->slab ? s->ghost_valid - k : 0;
+  *lo = s->top_edge ? 0 : -keep;
+  *hi = (int32_t)s->H + (s->bot_edge ? 0 : keep);
+}
+
+// Flip buffers after a k-step block, refresh the mirrored margins.
+int end_block(rd_sim* s, int k, int32_t lo, int32_t hi) {
+  const int out = s->cur ^ 1;
+  s->cur = out;
+  s->ghost_valid -= k;
+  return launch_mirror(s, s->u[out], s->v[out], nullptr, lo, hi);
+}
+
+int launch_tb(rd_sim* s, int k) {
+  if (s->slab && k > s->ghost_valid)
+    return set_err(s, RD_ERANGE, "slab ghost rows exhausted (k=%d > %d valid rows)", k, s->ghost_valid);
+  int32_t lo, hi;
+  block_rows(s, k, &lo, &hi);
+  if (int rc = launch_rows(s, k, s->cur, s->cur ^ 1, lo, hi)) return rc;
+  return end_block(s, k, lo, hi);
 }
 
 // a8: shared memory per CTA of cr_kernel with cs CTAs per cluster.
@@ -1353,6 +1372,63 @@ int rd_step_unchecked(rd_sim* s, int64_t n) {
   s->ghost_valid = (int32_t)s->halo;
   if (int rc = sync_probes(s)) return rc;
   return run_range(s, s->step + n, s->K);
+}
+
+// Slab blocks overlapped with the halo exchange: the
+// interior rows -- at least k rows from any exchanged ghost row -- depend only
+// on owned rows, so they run while the exchange is in flight; the edge bands
+// run once the ghosts have landed. Only a block that is one plain launch
+// qualifies (k <= the handle's depth, no stimulus due in it, no probe or
+// timelapse sample strictly inside); otherwise *started = 0 and the caller
+// steps with rd_step_unchecked after the exchange.
+int rd_step_begin(rd_sim* s, int64_t k, int32_t* started) {
+  if (!s || !started) return RD_EINVAL;
+  *started = 0;
+  if (!s->slab) return set_err(s, RD_EINVAL, "rd_step_begin: slab handles only");
+  if (s->pending_k) return set_err(s, RD_EINVAL, "rd_step_begin: a block is already open (rd_step_finish)");
+  if (k < 1 || k > s->halo) return set_err(s, RD_ERANGE, "k must be in [1, halo=%lld]", (long long)s->halo);
+  if (k > s->K || s->precise_mode) return RD_OK;
+  for (const auto& ev : s->events)
+    if (ev.at >= s->step && ev.at < s->step + k) return RD_OK;
+  for (int64_t t = s->step + 1; t < s->step + k; ++t) {
+    if (probe_due(s, t)) return RD_OK;
+    if (s->tl_stride > 0 && t % s->tl_stride == 0) return RD_OK;
+  }
+  if (int rc = sync_probes(s)) return rc;
+  s->ghost_valid = (int32_t)s->halo;
+  int32_t lo, hi;
+  block_rows(s, (int)k, &lo, &hi);
+  const int32_t a = s->top_edge ? 0 : (int32_t)k;
+  const int32_t b = (int32_t)s->H - (s->bot_edge ? 0 : (int32_t)k);
+  if (a < b)
+    if (int rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, a, b)) return rc;
+  s->pending_k = (int32_t)k;
+  *started = 1;
+  return RD_OK;
+}
+
+int rd_step_finish(rd_sim* s) {
+  if (!s) return RD_EINVAL;
+  if (!s->pending_k) return set_err(s, RD_EINVAL, "rd_step_finish: no open block (rd_step_begin)");
+  const int k = s->pending_k;
+  s->pending_k = 0;
+  int32_t lo, hi;
+  block_rows(s, k, &lo, &hi);
+  const int32_t a = s->top_edge ? 0 : k;
+  const int32_t b = (int32_t)s->H - (s->bot_edge ? 0 : k);
+  if (a < b) {
+    if (lo < a)
+      if (int rc = launch_rows(s, k, s->cur, s->cur ^ 1, lo, a)) return rc;
+    if (b < hi)
+      if (int rc = launch_rows(s, k, s->cur, s->cur ^ 1, b, hi)) return rc;
+  } else {
+    if (int rc = launch_rows(s, k, s->cur, s->cur ^ 1, lo, hi)) return rc;
+  }
+  if (int rc = end_block(s, k, lo, hi)) return rc;
+  s->step += k;
+  if (probe_due(s, s->step))
+    if (int rc = launch_probes(s, s->step)) return rc;
+  return RD_OK;
 }
 
 int rd_checkpoint(rd_sim* s) {

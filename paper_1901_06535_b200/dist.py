@@ -19,7 +19,7 @@ import numpy as np
 
 from . import RD_ENONFINITE, RDError, rd_checkpoint, rd_create_slab, rd_destroy, rd_get_stats, rd_probe_latch
 from . import rd_probe_result, rd_read_fields, rd_read_flags, rd_restore, rd_row_ptr, rd_set_stream, rd_step
-from . import rd_step_unchecked, rd_stimulate, rd_write_fields
+from . import rd_step_begin, rd_step_finish, rd_step_unchecked, rd_stimulate, rd_write_fields
 
 
 def slab_rows(H: int, world: int, rank: int) -> tuple[int, int]:
@@ -46,11 +46,12 @@ def exchange_plan(world: int, rank: int, rows: int, halo: int):
     return plan
 
 
-def exchange(tensors_by_peer, group=None):
-    """One halo exchange: tensors_by_peer = [(peer, [send...], [recv...])].
-    All sends/recvs are posted as one batch (an NCCL group) and waited on.
-    With NCCL, device rows go GPU to GPU over NVLink; with a CPU backend
-    (gloo: tests) device rows are staged through host tensors."""
+def exchange_post(tensors_by_peer, group=None):
+    """Post one halo exchange: tensors_by_peer = [(peer, [send...], [recv...])],
+    all sends/recvs as one batch (an NCCL group). With NCCL, device rows go
+    GPU to GPU over NVLink on NCCL's stream, ordered after the work already
+    queued on the current stream; with a CPU backend (gloo: tests) device rows
+    are staged through host tensors. Returns the pending exchange."""
     import torch
     import torch.distributed as dist
     staged = dist.get_backend(group) != "nccl" and any(
@@ -65,11 +66,23 @@ def exchange(tensors_by_peer, group=None):
             if staged:
                 landing.append((buf, r))
             ops.append(dist.P2POp(dist.irecv, buf, peer, group))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+    works = dist.batch_isend_irecv(ops) if ops else []
+    return works, landing
+
+
+def exchange_wait(pending):
+    """Complete a posted exchange: the current stream waits for it (NCCL), or
+    the staged rows land on the device (gloo)."""
+    works, landing = pending
+    for w in works:
+        w.wait()
     for buf, r in landing:
         r.copy_(buf)
+
+
+def exchange(tensors_by_peer, group=None):
+    """One halo exchange, posted and completed."""
+    exchange_wait(exchange_post(tensors_by_peer, group))
 
 
 class _DevRows:
@@ -156,11 +169,19 @@ class SlabSim:
         return out
 
     def exchange(self):
+        self.exchange_wait(self.exchange_post())
+
+    def exchange_post(self):
+        if self.world == 1 or not isinstance(self.transport, str):
+            return None
+        return [exchange_post(self.device_tensors(b), self.group) for b in range(self.batch)]
+
+    def exchange_wait(self, pending):
         if self.world == 1:
             return
         if isinstance(self.transport, str):
-            for b in range(self.batch):
-                exchange(self.device_tensors(b), self.group)
+            for p in pending:
+                exchange_wait(p)
         else:
             self.transport.exchange(self)
 
@@ -187,9 +208,17 @@ class SlabSim:
         rd_checkpoint(self.h)
         done = 0
         while done < n:
+            # the exchange of this block's input rows is in
+            # flight while the interior rows (which read no ghost row) run;
+            # the edge bands follow once the ghosts have landed
             k = min(self.halo, n - done)
-            self.exchange()
-            rd_step_unchecked(self.h, k)
+            pending = self.exchange_post()
+            started = rd_step_begin(self.h, k) if self.world > 1 else False
+            self.exchange_wait(pending)
+            if started:
+                rd_step_finish(self.h)
+            else:
+                rd_step_unchecked(self.h, k)
             done += k
         nonfinite, inexact = rd_read_flags(self.h)
         if not self.any_rank(nonfinite or inexact):
@@ -236,6 +265,8 @@ class LoopbackGroup:
         if len(self.arrived) < self.world:
             return
         self.arrived.clear()
+        import torch
+        torch.cuda.synchronize()  # every slab's queued work (its own stream) has produced the rows
         for b in range(self.slabs[0].batch):
             views = {r: dict((peer, (s, rv)) for peer, s, rv in sl.device_tensors(b)) for r, sl in self.slabs.items()}
             for r, peers in views.items():
@@ -256,11 +287,18 @@ class LoopbackGroup:
             rd_checkpoint(sl.h)
         done = 0
         while done < n:
+            # interior rows first, then the exchange (the interior launches
+            # finish before the copies land: a ghost read there would see stale
+            # rows and break the bitwise tests), then the edge bands
             k = min(halo, n - done)
+            started = [rd_step_begin(sl.h, k) for sl in slabs]
             for sl in slabs:
                 sl.exchange()
-            for sl in slabs:
-                rd_step_unchecked(sl.h, k)
+            for sl, st in zip(slabs, started):
+                if st:
+                    rd_step_finish(sl.h)
+                else:
+                    rd_step_unchecked(sl.h, k)
             done += k
         if not any(any(rd_read_flags(sl.h)) for sl in slabs):
             return

@@ -45,6 +45,12 @@ def test_virtual_slabs_equal_single_grid(G, halo, dtype, kernel):
     grp.step_all(steps)
     U = np.concatenate([s.read_owned(0)[0] for s in slabs])
     V = np.concatenate([s.read_owned(0)[1] for s in slabs])
+    # the blocks ran split (SURVEY.md §8(e) overlap): an interior slab
+    # launches interior + top band + bottom band per block, except the
+    # block holding the step-5 stimulus (one plain launch)
+    blocks = -(-steps // halo)
+    if G >= 3:
+        assert slabs[1].stats()["step_launches"] >= 3 * (blocks - 2) + 2
     for s in slabs:
         s.close()
 
