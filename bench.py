@@ -113,10 +113,17 @@ def dist_env():
     return world, rank, local
 
 
-def config_dict(world: int, T: int, tb_depth: int) -> dict:
+def config_dict(world: int, T: int, tb_depth: int, scaling: str = "weak") -> dict:
     """The `config` of the JSON line -- the same for our arm and the
     reference arm (BASELINE.json configs[3] at N = 1,
-    configs[4] weak scaling at N > 1)."""
+    configs[4] weak scaling at N > 1; --scaling strong: configs[4] at its full
+    65536 x 65536 over N GPUs)."""
+    if scaling == "strong":
+        d = {"workload": "configs[4] strong scaling: 65536x65536 fp32 row slabs over N GPUs, 256 obstacles "
+                         "phi=0.2, masked half-discs, NCCL halo exchange", "grid": [65536, 65536]}
+        return dict(d, time_steps_per_step=T, tb_depth=tb_depth,
+                    l2="inputs larger than L2 (5 planes of 17/N GB per GPU); no flush needed",
+                    parallelism=f"row slabs x{world}")
     if world == 1:
         d = {"workload": "configs[3] c4_roofline: 16384x16384 fp32, phi=0.054, u,v~U[0,0.1) seed 1, "
                          "64 half-discs r=8 seed 2, no-flux", "grid": [16384, 16384]}
@@ -172,7 +179,8 @@ def run_ours(args):
     T = args.timesteps
     hbm, hbm_src = peaks()
 
-    if world == 1:
+    strong = args.scaling == "strong"
+    if world == 1 and not strong:
         w = config(4)
         H, W = w.H, w.W
         # inputs built on the device: phi = 0.054, seeded U[0,0.1) noise
@@ -188,7 +196,9 @@ def run_ours(args):
         stepper = sim.step
         cells = H * W
     else:
-        w = config(5, H=16384 * world, W=16384, n_obstacles=16 * world)
+        # weak: 16384 rows per GPU; strong: the full 65536^2 grid split over
+        # the ranks (N = 1 included: one 120 GB slab)
+        w = (config(5) if strong else config(5, H=16384 * world, W=16384, n_obstacles=16 * world))
         H, W = w.H, w.W
         slab = SlabSim(W, H, rank, world, None, dtype=dtype, halo=max(args.tb, 4) if args.tb else 4)
         h = slab.h
@@ -200,7 +210,11 @@ def run_ours(args):
             slab.stimulate(shape, val, at)
         stepper = slab.step
         cells = slab.rows * W
-        u0, v0 = slab.read_owned(0)  # host copies of this rank's rows for the e2e leg
+        # host copies of this rank's rows for the e2e leg (not at the strong
+        # sizes: 17/N GB per plane)
+        u0 = v0 = None
+        if not strong:
+            u0, v0 = slab.read_owned(0)
     stream = torch.cuda.current_stream()
     rd.rd_set_stream(h, rd.stream_handle(stream))  # engine work on the stream the events are recorded on
 
@@ -263,7 +277,10 @@ def run_ours(args):
     # this rank's u, v from the host, steps, and reads u, v back (N > 1: the
     # owned rows of each slab; time = max over ranks)
     e2e = None
-    if args.e2e_steps > 0:
+    if strong:
+        e2e = {"skipped": "--scaling strong: 65536^2 host copies (17/N GB per plane) are not staged; "
+                          "the default (weak) line carries e2e"}
+    elif args.e2e_steps > 0:
         rows = u0.shape[0]
         pu = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
         pv = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
@@ -289,15 +306,15 @@ def run_ours(args):
                        "rd_read_fields(host); bytes per rank, time max over ranks")}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not strong and not args.no_cpu_baseline:
         cpu = cpu_baseline(u0, v0, phi, args.cpu_seconds)
 
     launches = st["launches"]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_dict(world, T, st["tb_depth"]),
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config_dict(world, T, st["tb_depth"], args.scaling),
                 "frac_of_one_step_hbm_roofline": value / world / (hbm / bpc),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
@@ -341,12 +358,13 @@ def run_reference(args):
     import oracle
     from rdinputs import config
     oracle.set_num_threads(host_cores())  # torchrun sets OMP_NUM_THREADS=1; rank 0 alone works here
-    if world == 1:
+    if world == 1 and args.scaling == "weak":
         w = config(4)
         sample = "4 time steps of the full 16384x16384 config-4 grid per bench step (after step 0's stimuli)"
     else:
         w = config(5, H=16384, W=16384, n_obstacles=16)
-        sample = "4 time steps of one 16384x16384 config-5 slab (rank 0's share) per bench step (after step 0)"
+        sample = ("4 time steps of one 16384x16384 slab of the config-5 geometry (16 obstacles) per bench step "
+                  "(after step 0); the metric is a per-cell rate")
     u, v = w.init_planes(0)
     phi = w.phi_plane(0).astype(np.float32)
     # untimed: step 0 with the stimuli (our arm stamps them before its timed
@@ -365,8 +383,8 @@ def run_reference(args):
     value = w.H * w.W * n * args.steps / el / 1e9
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": config_dict(world, args.timesteps, args.tb or 4),
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(world, args.timesteps, args.tb or 4, args.scaling),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": sample},
@@ -385,6 +403,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1 workload: configs[4] weak (16384 rows per GPU, default) or strong (65536^2 split)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
