@@ -219,10 +219,56 @@ int rd_checkpoint(struct rd_sim* sim);
  * The exchange reads rows [0, halo) and [rows-halo, rows) and writes the
  * ghost rows of the input buffer; the interior launch reads neither range's
  * ghosts and writes only the output buffer, so both may run concurrently.
- * Errors: RD_EINVAL (not a slab handle, block already open / not open),
- * RD_ERANGE (k), RD_ECUDA. */
-int rd_step_begin(struct rd_sim* sim, int64_t k, int32_t* started);
+ * flags: RD_BLOCK_PUSH -- peer-memory exchange: the
+ * block's edge bands also store their send rows (owned rows [0, halo) and
+ * [rows-halo, rows)) straight into the neighbours' ghost rows of their next
+ * input buffer (rd_set_peer), so no separate exchange follows the block;
+ * rd_step_finish first refreshes the mirrored columns of the ghost rows the
+ * neighbours stored into. Push blocks need k == halo (else *started = 0).
+ * The caller orders the ranks: between rd_step_begin and rd_step_finish the
+ * handle's stream must wait until both neighbours have finished the previous
+ * block (rd_stream_wait on a flag they rd_stream_signal after theirs).
+ * Errors: RD_EINVAL (not a slab handle, block already open / not open,
+ * RD_BLOCK_PUSH without registered neighbours), RD_ERANGE (k), RD_ECUDA. */
+#define RD_BLOCK_PUSH 1
+int rd_step_begin(struct rd_sim* sim, int64_t k, int32_t flags, int32_t* started);
 int rd_step_finish(struct rd_sim* sim);
+
+/* Peer-memory halo exchange, slab handles.
+ *   rd_plane_origins  this handle's (row 0, col 0) device pointers of u and v
+ *                     for both buffers, and its instance stride in bytes (to
+ *                     hand to the neighbours; on another GPU they map them
+ *                     with CUDA IPC).
+ *   rd_set_peer       register the neighbour above (side 0) or below (side 1)
+ *                     by those pointers (valid in this process), its owned
+ *                     rows (>= halo) and instance stride; the same width (and
+ *                     so the same row pitch) is assumed. u0 == NULL clears.
+ *   rd_push_ghosts    copy this handle's send rows of the current buffer
+ *                     (row storage, mirrored columns included) into the
+ *                     registered neighbours' ghost rows of their current
+ *                     buffer (the first exchange of a super-step).
+ *   rd_stream_signal  stream-ordered write of `value` to the 32-bit device
+ *                     word `flag` (e.g. a neighbour's, mapped here).
+ *   rd_stream_wait    the handle's stream waits until *flag >= value.
+ * Errors: RD_EINVAL (arguments, not a slab handle), RD_ECUDA. */
+int rd_plane_origins(const struct rd_sim* sim, void** u0, void** u1, void** v0, void** v1,
+                     int64_t* plane_stride_bytes);
+int rd_set_peer(struct rd_sim* sim, int32_t side, void* u0, void* u1, void* v0, void* v1, int64_t rows,
+                int64_t plane_stride_bytes);
+int rd_push_ghosts(struct rd_sim* sim);
+/* The handle's 32-bit flag word counting pushes received from the neighbour
+ * above (side 0) / below (side 1); it lives in the plane allocation, so a
+ * neighbour reaches it through the same IPC mapping. */
+int rd_flag_ptr(struct rd_sim* sim, int32_t side, void** flag);
+/* CUDA IPC of the plane allocation: export writes the 64-byte
+ * cudaIpcMemHandle and this process's base address; map opens a neighbour's
+ * handle here (peer access enabled lazily) and returns the mapped base -- a
+ * neighbour pointer p maps to mapped + (p - its base). Mappings close at
+ * rd_destroy. */
+int rd_ipc_export(struct rd_sim* sim, void* handle64, void** arena_base);
+int rd_ipc_map(struct rd_sim* sim, const void* handle64, void** mapped_base);
+int rd_stream_signal(struct rd_sim* sim, void* flag, uint32_t value);
+int rd_stream_wait(struct rd_sim* sim, void* flag, uint32_t value);
 int rd_step_unchecked(struct rd_sim* sim, int64_t n);
 int rd_read_flags(struct rd_sim* sim, int32_t* nonfinite, int32_t* inexact);
 int rd_restore(struct rd_sim* sim);

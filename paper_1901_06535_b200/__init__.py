@@ -21,7 +21,7 @@ from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_C
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
-           "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_step_begin", "rd_step_finish", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
+           "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_step_begin", "rd_step_finish", "RD_BLOCK_PUSH", "rd_plane_origins", "rd_set_peer", "rd_push_ghosts", "rd_flag_ptr", "rd_ipc_export", "rd_ipc_map", "rd_stream_signal", "rd_stream_wait", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -131,13 +131,70 @@ def rd_step_unchecked(h, n: int) -> None:
     _check(load().rd_step_unchecked(h, int(n)), h)
 
 
-def rd_step_begin(h, k: int) -> bool:
+RD_BLOCK_PUSH = 1
+
+
+def rd_step_begin(h, k: int, flags: int = 0) -> bool:
     """Open a slab block of k steps and launch its interior rows (they need
     no ghost rows) so they overlap the halo exchange; False: the block is not
-    one plain launch -- step it with rd_step_unchecked after the exchange."""
+    one plain launch -- step it with rd_step_unchecked after the exchange.
+    flags=RD_BLOCK_PUSH: the edge bands push their send rows into the
+    neighbours' ghost rows (peer memory) instead of a separate exchange."""
     started = C.c_int32(0)
-    _check(load().rd_step_begin(h, int(k), C.byref(started)), h)
+    _check(load().rd_step_begin(h, int(k), int(flags), C.byref(started)), h)
     return bool(started.value)
+
+
+def rd_plane_origins(h):
+    """((u0, u1), (v0, v1), instance stride bytes): this handle's (row 0,
+    col 0) device pointers of both buffers."""
+    p = [C.c_void_p() for _ in range(4)]
+    st = C.c_int64()
+    _check(load().rd_plane_origins(h, *[C.byref(x) for x in p], C.byref(st)), h)
+    return (p[0].value, p[1].value), (p[2].value, p[3].value), st.value
+
+
+def rd_set_peer(h, side: int, u, v, rows: int, stride_bytes: int) -> None:
+    """Register the slab neighbour above (side 0) / below (side 1) by its
+    plane origins (u = (u0, u1), v = (v0, v1)) valid in this process; u=None
+    clears."""
+    if u is None:
+        _check(load().rd_set_peer(h, int(side), None, None, None, None, 0, 0), h)
+    else:
+        _check(load().rd_set_peer(h, int(side), u[0], u[1], v[0], v[1], int(rows), int(stride_bytes)), h)
+
+
+def rd_push_ghosts(h) -> None:
+    _check(load().rd_push_ghosts(h), h)
+
+
+def rd_flag_ptr(h, side: int) -> int:
+    p = C.c_void_p()
+    _check(load().rd_flag_ptr(h, int(side), C.byref(p)), h)
+    return p.value
+
+
+def rd_ipc_export(h):
+    """(64-byte cudaIpcMemHandle, this process's base address of the plane allocation)."""
+    buf = C.create_string_buffer(64)
+    base = C.c_void_p()
+    _check(load().rd_ipc_export(h, buf, C.byref(base)), h)
+    return buf.raw, base.value
+
+
+def rd_ipc_map(h, handle64: bytes) -> int:
+    """Open a neighbour's exported handle here; returns the mapped base."""
+    base = C.c_void_p()
+    _check(load().rd_ipc_map(h, C.create_string_buffer(handle64, 64), C.byref(base)), h)
+    return base.value
+
+
+def rd_stream_signal(h, flag_ptr: int, value: int) -> None:
+    _check(load().rd_stream_signal(h, flag_ptr, int(value)), h)
+
+
+def rd_stream_wait(h, flag_ptr: int, value: int) -> None:
+    _check(load().rd_stream_wait(h, flag_ptr, int(value)), h)
 
 
 def rd_step_finish(h) -> None:

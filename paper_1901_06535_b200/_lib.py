@@ -68,8 +68,16 @@ SYMBOLS = [
     ("rd_step", C.c_int, [P, i64]),
     ("rd_checkpoint", C.c_int, [P]),
     ("rd_step_unchecked", C.c_int, [P, i64]),
-    ("rd_step_begin", C.c_int, [P, i64, C.POINTER(i32)]),
+    ("rd_step_begin", C.c_int, [P, i64, i32, C.POINTER(i32)]),
     ("rd_step_finish", C.c_int, [P]),
+    ("rd_plane_origins", C.c_int, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(i64)]),
+    ("rd_set_peer", C.c_int, [P, i32, P, P, P, P, i64, i64]),
+    ("rd_push_ghosts", C.c_int, [P]),
+    ("rd_flag_ptr", C.c_int, [P, i32, C.POINTER(P)]),
+    ("rd_ipc_export", C.c_int, [P, P, C.POINTER(P)]),
+    ("rd_ipc_map", C.c_int, [P, P, C.POINTER(P)]),
+    ("rd_stream_signal", C.c_int, [P, P, u32]),
+    ("rd_stream_wait", C.c_int, [P, P, u32]),
     ("rd_read_flags", C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     ("rd_restore", C.c_int, [P]),
     ("rd_get_step", C.c_int64, [P]),

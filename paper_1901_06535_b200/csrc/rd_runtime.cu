@@ -47,7 +47,8 @@ struct rd_sim {
   // tb_kernel input maps, one per input buffer (u[i], v[i], phi at a constant
   // stride; see alloc_planes)
   CUtensorMap tmap[2];
-  void* arena = nullptr;  // the plane allocation (u, v, phi, checkpoint)
+  void* arena = nullptr;  // the plane allocation (u, v, phi, checkpoint, push flags)
+  size_t arena_bytes = 0;
   rd_grid g{};
   rd_params p{};
   size_t esz = 4;
@@ -90,6 +91,17 @@ struct rd_sim {
   int64_t step = 0;
   int32_t ghost_valid = 0;  // slab: ghost rows still valid in the current buffers
   int32_t pending_k = 0;    // rd_step_begin opened a block of this many steps
+  std::vector<void*> ipc_mapped;  // peer arenas opened with rd_ipc_map (closed at destroy)
+  bool pending_push = false;  // ... with the peer-memory halo push
+  bool push_active = false;   // the launch being prepared pushes its send rows
+  // e: the slab neighbours above (0) / below (1) for the peer-memory push:
+  // their planes' (row 0, col 0) for both buffers, owned rows, instance stride
+  struct Peer {
+    void* u[2] = {nullptr, nullptr};
+    void* v[2] = {nullptr, nullptr};
+    int64_t rows = 0;
+    int64_t stride_bytes = 0;
+  } peer[2];
   int K = 4;
   std::vector<PendingEvent> events;
   std::vector<LatchedProbe> probes;
@@ -289,6 +301,27 @@ void fill_args(rd_sim* s, rdk::TBArgs<T>& a, int in, int out, int32_t out_lo, in
   a.fault_key = s->d_fault;
   a.precise_flag = s->d_precise;
   a.tl = (s->tl_stride > 0 && (s->step + K) % s->tl_stride == 0) ? origin<T>(s, s->tl) : nullptr;
+  a.push_up_u = a.push_up_v = a.push_dn_u = a.push_dn_v = nullptr;
+  a.push_stride_up = a.push_stride_dn = 0;
+  a.push_rows = 0;
+  a.pad3_ = 0;
+  if (s->push_active) {
+    // the neighbours' next input buffer has this launch's output parity
+    // (every rank launches the same blocks); row x lands in their ghost rows
+    const auto& up = s->peer[0];
+    const auto& dn = s->peer[1];
+    if (up.u[out]) {
+      a.push_up_u = static_cast<T*>(up.u[out]) + up.rows * s->pitch;
+      a.push_up_v = static_cast<T*>(up.v[out]) + up.rows * s->pitch;
+      a.push_stride_up = up.stride_bytes / (int64_t)sizeof(T);
+    }
+    if (dn.u[out]) {
+      a.push_dn_u = static_cast<T*>(dn.u[out]) - s->H * s->pitch;
+      a.push_dn_v = static_cast<T*>(dn.v[out]) - s->H * s->pitch;
+      a.push_stride_dn = dn.stride_bytes / (int64_t)sizeof(T);
+    }
+    a.push_rows = (int32_t)s->halo;
+  }
 }
 
 template <typename T, int K, bool REACT, int MODE>
@@ -910,8 +943,11 @@ int restore_checkpoint(rd_sim* s) {
 // segments with one TMA (tb_kernel). The checkpoint fills the two gaps.
 int alloc_planes(rd_sim* s) {
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
-  RD_CUDA(s, cudaMalloc(&s->arena, 7 * bytes));
-  RD_CUDA(s, cudaMemsetAsync(s->arena, 0, 7 * bytes, s->stream));
+  // + 256 bytes: the peer-push flag words (rd_flag_ptr), so one IPC handle
+  // of the arena maps planes and flags
+  RD_CUDA(s, cudaMalloc(&s->arena, 7 * bytes + 256));
+  RD_CUDA(s, cudaMemsetAsync(s->arena, 0, 7 * bytes + 256, s->stream));
+  s->arena_bytes = 7 * bytes + 256;
   char* base = static_cast<char*>(s->arena);
   s->u[0] = base;
   s->u[1] = base + 2 * bytes;
@@ -1247,6 +1283,7 @@ int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi
 int rd_destroy(rd_sim* s) {
   if (!s) return RD_OK;
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (void* m : s->ipc_mapped) cudaIpcCloseMemHandle(m);
   void* ps[] = {s->arena,   s->tl,    s->ck_tl,  s->d_probes, s->d_first, s->d_first_ck,
                 s->d_fault, s->d_flag, s->d_scratch, s->d_idx, s->d_pal, s->d_pal_n};
   for (void* p : ps)
@@ -1391,13 +1428,16 @@ int rd_step_unchecked(rd_sim* s, int64_t n) {
 // qualifies (k <= the handle's depth, no stimulus due in it, no probe or
 // timelapse sample strictly inside); otherwise *started = 0 and the caller
 // steps with rd_step_unchecked after the exchange.
-int rd_step_begin(rd_sim* s, int64_t k, int32_t* started) {
+int rd_step_begin(rd_sim* s, int64_t k, int32_t flags, int32_t* started) {
   if (!s || !started) return RD_EINVAL;
   *started = 0;
   if (!s->slab) return set_err(s, RD_EINVAL, "rd_step_begin: slab handles only");
   if (s->pending_k) return set_err(s, RD_EINVAL, "rd_step_begin: a block is already open (rd_step_finish)");
   if (k < 1 || k > s->halo) return set_err(s, RD_ERANGE, "k must be in [1, halo=%lld]", (long long)s->halo);
-  if (k > s->K || s->precise_mode) return RD_OK;
+  const bool push = (flags & RD_BLOCK_PUSH) != 0;
+  if (push && ((!s->top_edge && !s->peer[0].u[0]) || (!s->bot_edge && !s->peer[1].u[0])))
+    return set_err(s, RD_EINVAL, "rd_step_begin: RD_BLOCK_PUSH needs the neighbours registered (rd_set_peer)");
+  if (k > s->K || s->precise_mode || (push && k != s->halo)) return RD_OK;
   for (const auto& ev : s->events)
     if (ev.at >= s->step && ev.at < s->step + k) return RD_OK;
   for (int64_t t = s->step + 1; t < s->step + k; ++t) {
@@ -1413,6 +1453,7 @@ int rd_step_begin(rd_sim* s, int64_t k, int32_t* started) {
   if (a < b)
     if (int rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, a, b)) return rc;
   s->pending_k = (int32_t)k;
+  s->pending_push = push;
   *started = 1;
   return RD_OK;
 }
@@ -1421,23 +1462,149 @@ int rd_step_finish(rd_sim* s) {
   if (!s) return RD_EINVAL;
   if (!s->pending_k) return set_err(s, RD_EINVAL, "rd_step_finish: no open block (rd_step_begin)");
   const int k = s->pending_k;
+  const bool push = s->pending_push;
   s->pending_k = 0;
+  s->pending_push = false;
   int32_t lo, hi;
   block_rows(s, k, &lo, &hi);
   const int32_t a = s->top_edge ? 0 : k;
   const int32_t b = (int32_t)s->H - (s->bot_edge ? 0 : k);
-  if (a < b) {
-    if (lo < a)
-      if (int rc = launch_rows(s, k, s->cur, s->cur ^ 1, lo, a)) return rc;
-    if (b < hi)
-      if (int rc = launch_rows(s, k, s->cur, s->cur ^ 1, b, hi)) return rc;
-  } else {
-    if (int rc = launch_rows(s, k, s->cur, s->cur ^ 1, lo, hi)) return rc;
+  if (push) {
+    // the neighbours stored their send rows (interior columns) into this
+    // buffer's ghost rows: refresh those rows' mirrored ghost columns
+    const int32_t glo = s->top_edge ? 0 : -(int32_t)s->halo;
+    const int32_t ghi = (int32_t)s->H + (s->bot_edge ? 0 : (int32_t)s->halo);
+    if (int rc = launch_mirror(s, s->u[s->cur], s->v[s->cur], nullptr, glo, ghi)) return rc;
   }
-  if (int rc = end_block(s, k, lo, hi)) return rc;
+  // the edge bands hold every send row (k == halo on push blocks), so they
+  // alone push, after the caller's wait for the neighbours
+  s->push_active = push;
+  int rc = RD_OK;
+  if (a < b) {
+    if (lo < a) rc = launch_rows(s, k, s->cur, s->cur ^ 1, lo, a);
+    if (rc == RD_OK && b < hi) rc = launch_rows(s, k, s->cur, s->cur ^ 1, b, hi);
+  } else {
+    rc = launch_rows(s, k, s->cur, s->cur ^ 1, lo, hi);
+  }
+  s->push_active = false;
+  if (rc) return rc;
+  if (int rc2 = end_block(s, k, lo, hi)) return rc2;
   s->step += k;
   if (probe_due(s, s->step))
-    if (int rc = launch_probes(s, s->step)) return rc;
+    if (int rc3 = launch_probes(s, s->step)) return rc3;
+  return RD_OK;
+}
+
+int rd_set_peer(rd_sim* s, int32_t side, void* u0, void* u1, void* v0, void* v1, int64_t rows,
+                int64_t plane_stride_bytes) {
+  if (!s) return RD_EINVAL;
+  if (side != 0 && side != 1) return set_err(s, RD_EINVAL, "side must be 0 (above) or 1 (below)");
+  if (!s->slab) return set_err(s, RD_EINVAL, "rd_set_peer: slab handles only");
+  rd_sim::Peer& p = s->peer[side];
+  if (!u0) {
+    p = rd_sim::Peer{};
+    return RD_OK;
+  }
+  if (!u1 || !v0 || !v1 || rows < s->halo || plane_stride_bytes <= 0)
+    return set_err(s, RD_EINVAL, "rd_set_peer: four plane pointers, rows >= halo and a stride are required");
+  p.u[0] = u0, p.u[1] = u1, p.v[0] = v0, p.v[1] = v1;
+  p.rows = rows;
+  p.stride_bytes = plane_stride_bytes;
+  return RD_OK;
+}
+
+int rd_plane_origins(const rd_sim* s, void** u0, void** u1, void** v0, void** v1, int64_t* plane_stride_bytes) {
+  if (!s || !u0 || !u1 || !v0 || !v1) return RD_EINVAL;
+  auto org = [&](void* plane) { return static_cast<void*>(static_cast<char*>(plane) + (s->row_off * s->pitch + s->col_off) * s->esz); };
+  *u0 = org(s->u[0]);
+  *u1 = org(s->u[1]);
+  *v0 = org(s->v[0]);
+  *v1 = org(s->v[1]);
+  if (plane_stride_bytes) *plane_stride_bytes = s->plane_stride * (int64_t)s->esz;
+  return RD_OK;
+}
+
+int rd_flag_ptr(rd_sim* s, int32_t side, void** flag) {
+  if (!s || !flag || (side != 0 && side != 1)) return RD_EINVAL;
+  // word 0: pushes received from the neighbour above; word 1: from below
+  *flag = static_cast<char*>(s->arena) + s->arena_bytes - 256 + 4 * side;
+  return RD_OK;
+}
+
+int rd_ipc_export(rd_sim* s, void* handle64, void** arena_base) {
+  if (!s || !handle64 || !arena_base) return RD_EINVAL;
+  cudaIpcMemHandle_t h;
+  RD_CUDA(s, cudaIpcGetMemHandle(&h, s->arena));
+  std::memcpy(handle64, &h, sizeof h);
+  *arena_base = s->arena;
+  return RD_OK;
+}
+
+int rd_ipc_map(rd_sim* s, const void* handle64, void** mapped_base) {
+  if (!s || !handle64 || !mapped_base) return RD_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  RD_CUDA(s, cudaIpcOpenMemHandle(mapped_base, h, cudaIpcMemLazyEnablePeerAccess));
+  s->ipc_mapped.push_back(*mapped_base);
+  return RD_OK;
+}
+
+int rd_push_ghosts(rd_sim* s) {
+  if (!s) return RD_EINVAL;
+  if (!s->slab) return set_err(s, RD_EINVAL, "rd_push_ghosts: slab handles only");
+  const size_t row_bytes = (size_t)s->pitch * s->esz, col = (size_t)s->col_off * s->esz;
+  const size_t bytes = (size_t)s->halo * row_bytes;
+  for (int side = 0; side < 2; ++side) {
+    const rd_sim::Peer& p = s->peer[side];
+    if (!p.u[0]) continue;
+    // my rows [0, halo) -> the peer above's rows [rows, rows + halo); my rows
+    // [H - halo, H) -> the peer below's rows [-halo, 0) (row storage, ghost
+    // columns included)
+    const int64_t my_row = side == 0 ? 0 : s->H - s->halo;
+    const int64_t its_row = side == 0 ? p.rows : -s->halo;
+    for (int64_t b = 0; b < s->B; ++b)
+      for (int pl = 0; pl < 2; ++pl) {
+        char* src = plane_ptr(s, pl == 0 ? s->u[s->cur] : s->v[s->cur], b, my_row) - col;
+        char* dst = static_cast<char*>(pl == 0 ? p.u[s->cur] : p.v[s->cur]) + b * p.stride_bytes +
+                    its_row * (int64_t)row_bytes - (int64_t)col;
+        RD_CUDA(s, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s->stream));
+      }
+  }
+  return RD_OK;
+}
+
+// Stream-ordered 32-bit flag operations (driver stream memory operations,
+// reached through the runtime's entry-point query: no libcuda link).
+int rd_stream_signal(rd_sim* s, void* flag, uint32_t value) {
+  if (!s || !flag) return RD_EINVAL;
+  static PFN_cuStreamWriteValue32_v11070 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return set_err(s, RD_ECUDA, "cuStreamWriteValue32 entry point unavailable");
+    fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
+  }
+  if (fn(reinterpret_cast<CUstream>(s->stream), reinterpret_cast<CUdeviceptr>(flag), value, 0) != CUDA_SUCCESS)
+    return set_err(s, RD_ECUDA, "cuStreamWriteValue32 failed");
+  return RD_OK;
+}
+
+int rd_stream_wait(rd_sim* s, void* flag, uint32_t value) {
+  if (!s || !flag) return RD_EINVAL;
+  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return set_err(s, RD_ECUDA, "cuStreamWaitValue32 entry point unavailable");
+    fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(f);
+  }
+  if (fn(reinterpret_cast<CUstream>(s->stream), reinterpret_cast<CUdeviceptr>(flag), value,
+         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    return set_err(s, RD_ECUDA, "cuStreamWaitValue32 failed");
   return RD_OK;
 }
 

@@ -19,7 +19,9 @@ import numpy as np
 
 from . import RD_ENONFINITE, RDError, rd_checkpoint, rd_create_slab, rd_destroy, rd_get_stats, rd_probe_latch
 from . import rd_probe_result, rd_read_fields, rd_read_flags, rd_restore, rd_row_ptr, rd_set_stream, rd_step
-from . import rd_step_begin, rd_step_finish, rd_step_unchecked, rd_stimulate, rd_write_fields
+from . import RD_BLOCK_PUSH, rd_flag_ptr, rd_ipc_export, rd_ipc_map, rd_plane_origins, rd_push_ghosts, rd_set_peer
+from . import rd_step_begin, rd_step_finish, rd_step_unchecked, rd_stimulate, rd_stream_signal, rd_stream_wait
+from . import rd_write_fields
 
 
 def slab_rows(H: int, world: int, rank: int) -> tuple[int, int]:
@@ -106,7 +108,8 @@ class SlabSim:
     """
 
     def __init__(self, W: int, H: int, rank: int, world: int, phi_fn, *, dtype=np.float32, halo: int = 4,
-                 tb_depth: int = 0, batch: int = 1, transport="dist", group=None, params=None, flags: int = 0):
+                 tb_depth: int = 0, batch: int = 1, transport="dist", group=None, params=None, flags: int = 0,
+                 p2p: bool = False):
         self.W, self.H, self.rank, self.world, self.halo = W, H, rank, world, halo
         self.row0, self.rows = slab_rows(H, world, rank)
         if self.rows < halo and world > 1:
@@ -122,6 +125,8 @@ class SlabSim:
         self.transport = transport
         self.group = group
         self.plan = exchange_plan(world, rank, self.rows, halo)
+        self.p2p = bool(p2p) and world > 1
+        self.epoch = 0  # pushes done (peer-memory exchange): the neighbours count the same
         if not isinstance(transport, str):
             transport.register(self)
         else:
@@ -129,6 +134,49 @@ class SlabSim:
             # NCCL work is ordered against torch's current stream: issue the
             # engine's kernels on that stream too.
             self.set_stream(torch.cuda.current_stream())
+            if self.p2p:
+                self._wire_peers()
+
+    # ---- peer-memory exchange across GPUs (opt-in) ----
+    # Each rank exports its plane allocation (CUDA IPC), maps its neighbours',
+    # and registers their plane origins (rd_set_peer): a block's edge launch
+    # then stores the send rows straight into the neighbours' ghost rows.
+    # Ranks are ordered by stream-ordered counters in the same allocations:
+    # after a push a rank adds one to each neighbour's word (rd_stream_signal);
+    # before using ghost rows it waits for its own words (rd_stream_wait).
+    # Not exercised on a one-GPU box (ranks must not wait on one another on a
+    # shared GPU); LoopbackGroup(p2p=True) tests the same data path in one
+    # process.
+    def _wire_peers(self):
+        import torch.distributed as dist
+        handle, base = rd_ipc_export(self.h)
+        (u0, u1), (v0, v1), stride = rd_plane_origins(self.h)
+        mine = dict(handle=handle, base=base, u=(u0, u1), v=(v0, v1), stride=stride, rows=self.rows,
+                    flags=(rd_flag_ptr(self.h, 0), rd_flag_ptr(self.h, 1)))
+        every = [None] * self.world
+        dist.all_gather_object(every, mine, group=self.group)
+        self.peer_flags = {}
+        for side, peer in ((0, self.rank - 1), (1, self.rank + 1)):
+            if not 0 <= peer < self.world:
+                continue
+            d = every[peer]
+            mapped = rd_ipc_map(self.h, d["handle"])
+            rel = lambda p: mapped + (p - d["base"])  # noqa: E731
+            rd_set_peer(self.h, side, (rel(d["u"][0]), rel(d["u"][1])), (rel(d["v"][0]), rel(d["v"][1])),
+                        d["rows"], d["stride"])
+            # my pushes arrive at the neighbour above as "from below" (its
+            # word 1), at the neighbour below as "from above" (its word 0)
+            self.peer_flags[side] = rel(d["flags"][1 - side])
+        self.my_flags = {side: rd_flag_ptr(self.h, side) for side in self.peer_flags}
+
+    def _signal(self):
+        self.epoch += 1
+        for f in self.peer_flags.values():
+            rd_stream_signal(self.h, f, self.epoch)
+
+    def _wait(self):
+        for f in self.my_flags.values():
+            rd_stream_wait(self.h, f, self.epoch)
 
     def close(self):
         if self.h:
@@ -206,6 +254,48 @@ class SlabSim:
         if n <= 0:
             return
         rd_checkpoint(self.h)
+        if self.p2p and isinstance(self.transport, str):
+            self._step_p2p(n)
+        else:
+            self._step_exchange(n)
+        nonfinite, inexact = rd_read_flags(self.h)
+        if not self.any_rank(nonfinite or inexact):
+            return
+        self._replay(n)
+
+    def _step_p2p(self, n: int):
+        """Blocks with the peer-memory push: the edge launches store the send
+        rows into the neighbours' next input buffer. A block that is not a
+        push block (a stimulus in it, a partial block) first re-pushes the
+        send rows in full row storage -- the kernel pushes carry the interior
+        columns only, whose mirrored ghost columns rd_step_finish refreshes --
+        and steps plainly."""
+        rd_push_ghosts(self.h)
+        self._signal()
+        done = 0
+        while done < n:
+            k = min(self.halo, n - done)
+            started = rd_step_begin(self.h, k, RD_BLOCK_PUSH)
+            self._wait()  # the neighbours' previous push has landed
+            if started:
+                rd_step_finish(self.h)
+                self._signal()
+            else:
+                # full-row re-push (mirrored columns) for this block, step,
+                # then -- once every neighbour has stepped too (a partial
+                # block rewrites its kept ghost rows) -- push the new buffer's
+                # send rows for the next block
+                rd_push_ghosts(self.h)
+                self._signal()
+                self._wait()
+                rd_step_unchecked(self.h, k)
+                self._signal()
+                self._wait()
+                rd_push_ghosts(self.h)
+                self._signal()
+            done += k
+
+    def _step_exchange(self, n: int):
         done = 0
         while done < n:
             # SURVEY.md §8(e): the exchange of this block's input rows is in
@@ -220,9 +310,8 @@ class SlabSim:
             else:
                 rd_step_unchecked(self.h, k)
             done += k
-        nonfinite, inexact = rd_read_flags(self.h)
-        if not self.any_rank(nonfinite or inexact):
-            return
+
+    def _replay(self, n: int):
         rd_restore(self.h)
         for _ in range(n):
             self.exchange()
@@ -252,13 +341,26 @@ class LoopbackGroup:
     once every slab has finished its block. Used to test the decomposition
     bitwise on a single GPU."""
 
-    def __init__(self, world: int):
+    def __init__(self, world: int, p2p: bool = False):
         self.world = world
+        self.p2p = p2p
         self.slabs = {}
         self.arrived = set()
 
     def register(self, slab: SlabSim):
         self.slabs[slab.rank] = slab
+        if self.p2p and len(self.slabs) == self.world:
+            # peer-memory exchange emulated in one process: every virtual rank
+            # on one stream (serial order replaces the cross-rank flags), each
+            # registered with its neighbours' plane origins
+            import torch
+            for sl in self.slabs.values():
+                sl.set_stream(torch.cuda.current_stream())
+            for r, sl in self.slabs.items():
+                for side, peer in ((0, r - 1), (1, r + 1)):
+                    if 0 <= peer < self.world:
+                        u, v, stride = rd_plane_origins(self.slabs[peer].h)
+                        rd_set_peer(sl.h, side, u, v, self.slabs[peer].rows, stride)
 
     def exchange(self, slab: SlabSim):
         self.arrived.add(slab.rank)
@@ -285,6 +387,37 @@ class LoopbackGroup:
         halo = slabs[0].halo
         for sl in slabs:
             rd_checkpoint(sl.h)
+        if self.p2p:
+            self._step_all_p2p(slabs, n, halo)
+        else:
+            self._step_all_exchange(slabs, n, halo)
+        if not any(any(rd_read_flags(sl.h)) for sl in slabs):
+            return
+        self._replay_all(slabs, n)
+
+    def _step_all_p2p(self, slabs, n, halo):
+        """SlabSim._step_p2p over the virtual ranks, in serial order on one
+        stream: pushes land in the neighbours' next input buffers."""
+        for sl in slabs:
+            rd_push_ghosts(sl.h)
+        done = 0
+        while done < n:
+            k = min(halo, n - done)
+            started = [rd_step_begin(sl.h, k, RD_BLOCK_PUSH) for sl in slabs]
+            assert all(started) or not any(started), "ranks disagree on a push block"
+            if started[0]:
+                for sl in slabs:
+                    rd_step_finish(sl.h)
+            else:
+                for sl in slabs:
+                    rd_push_ghosts(sl.h)  # full rows: mirrored columns too
+                for sl in slabs:
+                    rd_step_unchecked(sl.h, k)
+                for sl in slabs:
+                    rd_push_ghosts(sl.h)  # the new buffer's ghosts, for the next block
+            done += k
+
+    def _step_all_exchange(self, slabs, n, halo):
         done = 0
         while done < n:
             # interior rows first, then the exchange (the interior launches
@@ -300,8 +433,8 @@ class LoopbackGroup:
                 else:
                     rd_step_unchecked(sl.h, k)
             done += k
-        if not any(any(rd_read_flags(sl.h)) for sl in slabs):
-            return
+
+    def _replay_all(self, slabs, n):
         for sl in slabs:
             rd_restore(sl.h)
         for _ in range(n):
