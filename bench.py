@@ -200,7 +200,8 @@ def run_ours(args):
         # the ranks (N = 1 included: one 120 GB slab)
         w = (config(5) if strong else config(5, H=16384 * world, W=16384, n_obstacles=16 * world))
         H, W = w.H, w.W
-        slab = SlabSim(W, H, rank, world, None, dtype=dtype, halo=max(args.tb, 4) if args.tb else 4)
+        slab = SlabSim(W, H, rank, world, None, dtype=dtype, halo=max(args.tb, 4) if args.tb else 4,
+                       p2p=args.p2p)
         h = slab.h
         rd.rd_paint_phi(h, -1, None, 0.054)
         for rect in w.meta["obstacles"]:
@@ -403,6 +404,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--p2p", action="store_true",
+                    help="N > 1: peer-memory halo push (CUDA IPC + stream-ordered flags) instead of NCCL")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="N > 1 workload: configs[4] weak (16384 rows per GPU, default) or strong (65536^2 split)")
     args = ap.parse_args()
