@@ -17,6 +17,7 @@ flush is needed between steps. Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -251,11 +252,13 @@ def run_ours(args):
     k_launches = max(1, st["timed_launches"])
     bpc = BYTES_PER_CELL[dtype]
     achieved = bpc * st["cell_updates"] / (kms / 1e3) / 1e9 if kms > 0 else None
+    # DRAM bytes per tb_kernel launch from the latest committed ncu --set full
+    # capture (profiles/traffic_rNN.json, scripts/summarize_ncu.py)
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tpath):
+    tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))
+    if tfiles:
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tfiles[-1])).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     # temporal blocking moves the kernel off the HBM roof (DRAM bytes per
