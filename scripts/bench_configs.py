@@ -23,6 +23,13 @@ import paper_1901_06535_b200 as rd  # noqa: E402
 from rdinputs import config  # noqa: E402
 
 
+def hbm_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
 def run(n, dtype, tb):
     w = config(n, dtype=dtype)
     if n in (4, 5):
@@ -59,8 +66,13 @@ def run(n, dtype, tb):
     fires = [[sim.probe_result(p) for p in ps] for ps in pids]
     cells = w.B * w.H * w.W * w.steps
     sim.close()
+    gcells = cells / (ms / 1e3) / 1e9
+    # one-step HBM roofline: read u, v, phi + write u, v = 20 B (fp32) / 40 B
+    # (fp64) per cell-update at the measured copy bandwidth
+    roof = hbm_gbs() / (20 if np.dtype(dtype).itemsize == 4 else 40)
     return {"config": w.name, "dtype": np.dtype(dtype).name, "B": w.B, "H": w.H, "W": w.W, "steps": w.steps,
-            "device_ms": ms, "wall_s": wall, "gcell_updates_per_s": cells / (ms / 1e3) / 1e9,
+            "device_ms": ms, "wall_s": wall, "gcell_updates_per_s": gcells,
+            "frac_of_one_step_hbm_roofline": gcells / roof, "stencil_kernel": ["tb", "lp", "cr"][st["kernel"]],
             "launches": st["launches"], "step_launches": st["step_launches"], "tb_depth": st["tb_depth"],
             "first_fire": fires, "expect": w.expect.get("fires")}
 
