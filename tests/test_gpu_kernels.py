@@ -198,3 +198,21 @@ def test_cluster_resident_palette_layout(dtype, monkeypatch):
     s3.close()
     ref3 = oracle.run(u0, v0, rough, 12)
     assert np.array_equal(u3, ref3.u) and np.array_equal(v3, ref3.v)
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    """The boundary used from C, without Python: tests/c/abi_c_demo.c links
+    librd.so (and, as a test, the oracle's C library), runs a two-instance
+    fp64 and fp32 batch through rd_create / rd_stimulate / rd_step /
+    rd_read_fields / rd_probe and compares with the oracle bitwise, plus
+    error codes (RD_EINVAL, RD_ERANGE)."""
+    import subprocess
+    root = os.path.dirname(HERE)
+    exe = str(tmp_path / "abi_c_demo")
+    lib, orc = os.path.join(root, "paper_1901_06535_b200"), os.path.join(root, "oracle")
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(root, "include"), "-I", orc,
+                    os.path.join(HERE, "c", "abi_c_demo.c"), "-L", lib, "-lrd", "-L", orc, "-lorc",
+                    f"-Wl,-rpath,{lib}:{orc}", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "C ABI ok" in out.stdout
