@@ -64,6 +64,8 @@ struct rd_sim {
   int cr_cs = 0;        // CTAs per cluster for cr_kernel
   size_t cr_smem = 0;   // its dynamic shared memory per CTA
   bool cr_pal = false;  // cr_kernel with phi as palette indices
+  bool margins_stale = false;   // u/v mirror margins not refreshed since a cr_kernel launch
+  int64_t probes_done_at = -1;  // the step whose probes a cr_kernel launch evaluated
   std::vector<std::vector<double>> pal;  // distinct phi values per instance (cr PAL layout)
   bool pal_ok = true;     // every instance has <= 256
   bool pal_dirty = true;  // device palette / index plane need a rebuild
@@ -458,7 +460,15 @@ int end_block(rd_sim* s, int k, int32_t lo, int32_t hi) {
   return launch_mirror(s, s->u[out], s->v[out], nullptr, lo, hi);
 }
 
+// Refresh the u/v mirror margins if a cr_kernel launch left them stale.
+int fresh_margins(rd_sim* s) {
+  if (!s->margins_stale) return RD_OK;
+  s->margins_stale = false;
+  return launch_mirror(s, s->u[s->cur], s->v[s->cur], nullptr, 0, (int32_t)s->H);
+}
+
 int launch_tb(rd_sim* s, int k) {
+  if (int rc = fresh_margins(s)) return rc;
   if (s->slab && k > s->ghost_valid)
     return set_err(s, RD_ERANGE, "slab ghost rows exhausted (k=%d > %d valid rows)", k, s->ghost_valid);
   int32_t lo, hi;
@@ -468,6 +478,8 @@ int launch_tb(rd_sim* s, int k) {
 }
 
 // a8: shared memory per CTA of cr_kernel with cs CTAs per cluster.
+bool probe_due(const rd_sim* s, int64_t step);
+
 // a8: shared memory per CTA of cr_kernel with cs CTAs per cluster, phi as
 // values (pal = false) or as palette indices (pal = true).
 size_t cr_smem_bytes(const rd_sim* s, int cs, bool pal) {
@@ -502,6 +514,11 @@ cudaError_t launch_cr_t(rd_sim* s, int64_t n, size_t smem, int cs, bool query, i
   ca.a.hb = 0;
   ca.idx = s->d_idx;
   ca.pal = static_cast<const T*>(s->d_pal);
+  ca.probes = s->d_probes;
+  ca.first_fire = s->d_first;
+  ca.n_probes = (int32_t)s->probes.size();
+  ca.probe_step = (!s->probes.empty() && probe_due(s, s->step + n)) ? s->step + n : -1;
+  ca.pad_ = 0;
   ca.cs = cs;
   ca.n = (int32_t)n;
   return cudaLaunchKernelEx(&cfg, fn, ca);
@@ -636,7 +653,10 @@ void palette_add(rd_sim* s, int64_t b, double value) {
   s->pal_dirty = true;
 }
 
-// One cluster-resident launch of n steps, then the global mirrors.
+// One cluster-resident launch of n steps. It evaluates the probes due at its
+// last step and needs no global mirror margins (it mirrors from the band), so
+// none are refreshed after it: the margins are marked stale and the next
+// consumer that reads them (tb/lp launches) refreshes them first.
 int launch_cr(rd_sim* s, int64_t n) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (s->profiling) {
@@ -656,7 +676,8 @@ int launch_cr(rd_sim* s, int64_t n) {
   cudaError_t e = cr_dispatch(s, s->cr_pal, n, s->cr_smem, s->cr_cs, false, nullptr);
   if (e != cudaSuccess) return set_err(s, RD_ECUDA, "cr_kernel launch: %s", cudaGetErrorString(e));
   if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
-  if (int rc = launch_mirror(s, s->u[s->cur], s->v[s->cur], nullptr, 0, (int32_t)s->H)) return rc;
+  s->margins_stale = true;
+  if (!s->probes.empty() && probe_due(s, s->step + n)) s->probes_done_at = s->step + n;
   s->st.launches++;
   s->st.step_launches++;
   s->st.cell_updates += s->B * s->H * s->W * n;
@@ -782,6 +803,7 @@ int run_blocks(rd_sim* s, int64_t next, int kmax) {
     s->step = next;
     return RD_OK;
   }
+  if (int rc = fresh_margins(s)) return rc;  // outside any graph capture
   const bool graph = !(s->g.flags & RD_NO_GRAPH) && !s->profiling && !s->slab && !s->precise_mode &&
                      !s->graphs_broken && next - s->step >= 2 * kmax;
   if (!graph) {
@@ -880,7 +902,7 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
       if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
     if (s->tl_stride > 0) next = std::min(next, (s->step / s->tl_stride + 1) * (int64_t)s->tl_stride);
     if ((rc = run_blocks(s, next, kmax))) return rc;
-    if (probe_due(s, s->step))
+    if (probe_due(s, s->step) && s->probes_done_at != s->step)
       if ((rc = launch_probes(s, s->step))) return rc;
   }
   return RD_OK;
@@ -933,6 +955,8 @@ int restore_checkpoint(rd_sim* s) {
   s->events = s->ck_events;
   s->step = s->ck_step;
   s->ghost_valid = (int32_t)s->halo;
+  s->margins_stale = true;  // the checkpoint copy may predate a refresh
+  s->probes_done_at = -1;
   return reset_fault(s);
 }
 
