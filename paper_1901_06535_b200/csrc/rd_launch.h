@@ -1,0 +1,34 @@
+// rd_launch.h — the stencil-kernel launchers, instantiated in their own
+// translation units (rd_launch_tb_f32.cu, rd_launch_tb_f64.cu,
+// rd_launch_cr.cu) so the heavy template instantiations compile in parallel.
+// The runtime (rd_runtime.cu) computes the arguments and the launch geometry.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "rd_kernels.cuh"
+
+namespace rdl {
+
+// mode: rdk::MODE_*; react: reaction on (else diffusion only, MODE_PRECISE);
+// lp: the level-parallel variant (K <= 4; CTAs of 32*K threads), else
+// tb_kernel (one-warp CTAs). An unsupported combination returns
+// cudaErrorInvalidValue.
+int occupancy_tb_f32(int K, int mode, bool react, bool lp);  // resident CTAs per SM (>= 1)
+int occupancy_tb_f64(int K, int mode, bool react, bool lp);
+inline int occupancy_tb(bool f32, int K, int mode, bool react, bool lp) {
+  return f32 ? occupancy_tb_f32(K, mode, react, lp) : occupancy_tb_f64(K, mode, react, lp);
+}
+cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, unsigned grid,
+                      cudaStream_t st);
+cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react, bool lp, unsigned grid,
+                      cudaStream_t st);
+
+// cr_kernel over `batch` clusters of cs CTAs with `smem` dynamic shared memory
+// (pal: phi as palette indices). query: return the co-resident cluster count
+// in *clusters instead of launching.
+cudaError_t launch_cr(const rdk::CrArgs<float>& a, int mode, bool react, bool pal, int cs, unsigned batch,
+                      size_t smem, cudaStream_t st, bool query, int* clusters);
+cudaError_t launch_cr(const rdk::CrArgs<double>& a, int mode, bool react, bool pal, int cs, unsigned batch,
+                      size_t smem, cudaStream_t st, bool query, int* clusters);
+
+}  // namespace rdl

@@ -1,0 +1,10 @@
+// tb_kernel / lp_kernel instantiations and their occupancy, fp32 (see rd_launch.h).
+#include "rd_launch_tb.cuh"
+
+namespace rdl {
+cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, unsigned grid,
+                      cudaStream_t st) {
+  return detail::dispatch<float>(a, K, mode, react, lp, grid, st, nullptr);
+}
+int occupancy_tb_f32(int K, int mode, bool react, bool lp) { return detail::occupancy<float>(K, mode, react, lp); }
+}  // namespace rdl

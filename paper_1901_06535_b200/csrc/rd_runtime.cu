@@ -21,6 +21,7 @@
 
 #include "../../include/rd.h"
 #include "rd_kernels.cuh"
+#include "rd_launch.h"
 
 namespace {
 
@@ -326,73 +327,23 @@ void fill_args(rd_sim* s, rdk::TBArgs<T>& a, int in, int out, int32_t out_lo, in
   }
 }
 
-template <typename T, int K, bool REACT, int MODE>
-cudaError_t launch_tb_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_hi) {
+// One tb_kernel (or lp_kernel) launch: the strip geometry, a persistent grid
+// of as many CTAs as can be resident (occupancy API) capped by the number of
+// tasks, and the row-block height (pick_hb). The kernels are instantiated in
+// rd_launch_tb_*.cu.
+template <typename T>
+cudaError_t launch_stencil(rd_sim* s, int k, int in, int out, int32_t out_lo, int32_t out_hi, int mode, bool react) {
   constexpr int V = vec_of<T>();
-  using G = rdk::StripGeom<K, V>;
+  const bool lp = s->use_lp && k <= 4;
+  const int hx = ((k + V - 1) / V) * V, wo = 32 * V - 2 * hx;  // rdk::StripGeom<K, V>
   rdk::TBArgs<T> a;
-  fill_args<T>(s, a, in, out, out_lo, out_hi, K);
-  a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
-  // persistent grid of one-warp CTAs: as many as can be resident (occupancy
-  // API), capped by the number of tasks
-  static int per_sm = 0;
-  if (!per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdk::tb_kernel<T, K, V, REACT, MODE>, 32, 0) !=
-            cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-  }
-  const int64_t ctas = (int64_t)s->num_sms * per_sm;
-  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, K, ctas);
+  fill_args<T>(s, a, in, out, out_lo, out_hi, k);
+  a.n_strips = (int32_t)((s->W + wo - 1) / wo);
+  const int64_t ctas = (int64_t)s->num_sms * rdl::occupancy_tb(sizeof(T) == 4, k, mode, react, lp);
+  // lp: a task costs ~hb + 3K rows
+  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, lp ? k + (k + 1) / 2 : k, ctas);
   const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
-  const int64_t grid = std::min<int64_t>(tasks, ctas);
-  rdk::tb_kernel<T, K, V, REACT, MODE><<<(unsigned)grid, 32, 0, s->stream>>>(a);
-  return cudaGetLastError();
-}
-
-// Level-parallel variant for small (L2-resident) grids: CTAs of K warps.
-template <typename T, int K, bool REACT, int MODE>
-cudaError_t launch_lp_t(rd_sim* s, int in, int out, int32_t out_lo, int32_t out_hi) {
-  constexpr int V = vec_of<T>();
-  using G = rdk::StripGeom<K, V>;
-  rdk::TBArgs<T> a;
-  fill_args<T>(s, a, in, out, out_lo, out_hi, K);
-  a.n_strips = (int32_t)((s->W + G::WO - 1) / G::WO);
-  static int per_sm = 0;
-  if (!per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdk::lp_kernel<T, K, V, REACT, MODE>, 32 * K, 0) !=
-            cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-  }
-  const int64_t ctas = (int64_t)s->num_sms * per_sm;
-  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, K + (K + 1) / 2, ctas);  // task ~ hb + 3K rows
-  const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
-  rdk::lp_kernel<T, K, V, REACT, MODE><<<(unsigned)std::min<int64_t>(tasks, ctas), 32 * K, 0, s->stream>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename T, bool REACT, int MODE>
-cudaError_t launch_tb_k(rd_sim* s, int k, int in, int out, int32_t lo, int32_t hi) {
-  if (s->use_lp && k <= 4) {
-    switch (k) {
-      case 1: return launch_lp_t<T, 1, REACT, MODE>(s, in, out, lo, hi);
-      case 2: return launch_lp_t<T, 2, REACT, MODE>(s, in, out, lo, hi);
-      case 3: return launch_lp_t<T, 3, REACT, MODE>(s, in, out, lo, hi);
-      case 4: return launch_lp_t<T, 4, REACT, MODE>(s, in, out, lo, hi);
-    }
-  }
-  switch (k) {
-    case 1: return launch_tb_t<T, 1, REACT, MODE>(s, in, out, lo, hi);
-    case 2: return launch_tb_t<T, 2, REACT, MODE>(s, in, out, lo, hi);
-    case 3: return launch_tb_t<T, 3, REACT, MODE>(s, in, out, lo, hi);
-    case 4: return launch_tb_t<T, 4, REACT, MODE>(s, in, out, lo, hi);
-    case 5: return launch_tb_t<T, 5, REACT, MODE>(s, in, out, lo, hi);
-    case 6: return launch_tb_t<T, 6, REACT, MODE>(s, in, out, lo, hi);
-    case 7: return launch_tb_t<T, 7, REACT, MODE>(s, in, out, lo, hi);
-    case 8: return launch_tb_t<T, 8, REACT, MODE>(s, in, out, lo, hi);
-  }
-  return cudaErrorInvalidValue;
+  return rdl::launch_tb(a, k, mode, react, lp, (unsigned)std::min<int64_t>(tasks, ctas), s->stream);
 }
 
 // One stencil launch of k steps from buffer `in` to `out` producing rows
@@ -413,28 +364,12 @@ int launch_rows(rd_sim* s, int k, int in, int out, int32_t lo, int32_t hi) {
     ++s->ev_used;
     RD_CUDA(s, cudaEventRecord(e0, s->stream));
   }
-  cudaError_t e;
-  // the fast modes (exact rewrites + guarded fp32 division) unless this is a
-  // precise replay or there is no checkpoint to replay from
+  // the fast modes (exact rewrites + certified fp32 division) unless this is
+  // a precise replay or there is no checkpoint to replay from
   const bool precise = s->precise_mode || (s->g.flags & RD_NO_CHECKPOINT) || s->fast_mode == rdk::MODE_PRECISE;
-  if (s->esz == 4) {
-    if (!react)
-      e = launch_tb_k<float, false, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
-    else if (precise)
-      e = launch_tb_k<float, true, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
-    else if (s->fast_mode == rdk::MODE_FOLD_DIV4_NG)
-      e = launch_tb_k<float, true, rdk::MODE_FOLD_DIV4_NG>(s, k, in, out, lo, hi);
-    else if (s->fast_mode == rdk::MODE_FOLD_DIV4)
-      e = launch_tb_k<float, true, rdk::MODE_FOLD_DIV4>(s, k, in, out, lo, hi);
-    else
-      e = launch_tb_k<float, true, rdk::MODE_FOLD>(s, k, in, out, lo, hi);
-  } else {
-    if (!react)
-      e = launch_tb_k<double, false, rdk::MODE_PRECISE>(s, k, in, out, lo, hi);
-    else
-      e = precise ? launch_tb_k<double, true, rdk::MODE_PRECISE>(s, k, in, out, lo, hi)
-                  : launch_tb_k<double, true, rdk::MODE_FOLD>(s, k, in, out, lo, hi);
-  }
+  const int mode = (!react || precise) ? rdk::MODE_PRECISE : s->fast_mode;
+  const cudaError_t e = s->esz == 4 ? launch_stencil<float>(s, k, in, out, lo, hi, mode, react)
+                                    : launch_stencil<double>(s, k, in, out, lo, hi, mode, react);
   if (e != cudaSuccess) return set_err(s, RD_ECUDA, "tb_kernel<k=%d> launch: %s", k, cudaGetErrorString(e));
   if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
   s->st.launches++;
@@ -488,59 +423,33 @@ size_t cr_smem_bytes(const rd_sim* s, int cs, bool pal) {
   return (size_t)(rdk::cr_layout_elems(rows, w4, V, pal) * (int64_t)s->esz + (pal ? rows * w4 * V : 0));
 }
 
-template <typename T, bool REACT, int MODE, bool PAL>
-cudaError_t launch_cr_t(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
-  constexpr int nt = rdk::cr_threads<T>();
-  auto fn = rdk::cr_kernel<T, REACT, MODE, nt, PAL>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3((unsigned)cs, (unsigned)s->B, 1);
-  cfg.blockDim = dim3((unsigned)nt, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s->stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (query) return cudaOccupancyMaxActiveClusters(clusters, fn, &cfg);
+// One cr_kernel launch of n steps (or, query, the co-resident cluster count);
+// the kernels are instantiated in rd_launch_cr.cu.
+template <typename T>
+cudaError_t launch_cr_t(rd_sim* s, bool pal, int64_t n, size_t smem, int cs, bool query, int* clusters) {
   rdk::CrArgs<T> ca;
-  fill_args<T>(s, ca.a, s->cur, s->cur, 0, (int32_t)s->H, (int)n);
-  ca.a.n_strips = 0;
-  ca.a.hb = 0;
-  ca.idx = s->d_idx;
-  ca.pal = static_cast<const T*>(s->d_pal);
-  ca.probes = s->d_probes;
-  ca.first_fire = s->d_first;
-  ca.n_probes = (int32_t)s->probes.size();
-  ca.probe_step = (!s->probes.empty() && probe_due(s, s->step + n)) ? s->step + n : -1;
-  ca.pad_ = 0;
-  ca.cs = cs;
-  ca.n = (int32_t)n;
-  return cudaLaunchKernelEx(&cfg, fn, ca);
-}
-
-template <typename T, bool PAL>
-cudaError_t launch_cr_mode(rd_sim* s, int64_t n, size_t smem, int cs, bool query, int* clusters) {
-  if (s->g.flags & RD_REACTION_OFF)
-    return launch_cr_t<T, false, rdk::MODE_PRECISE, PAL>(s, n, smem, cs, query, clusters);
-  if (sizeof(T) == 4 && s->fast_mode == rdk::MODE_FOLD_DIV4_NG)
-    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4_NG, PAL>(s, n, smem, cs, query, clusters);
-  if (sizeof(T) == 4 && s->fast_mode == rdk::MODE_FOLD_DIV4)
-    return launch_cr_t<T, true, rdk::MODE_FOLD_DIV4, PAL>(s, n, smem, cs, query, clusters);
-  return launch_cr_t<T, true, rdk::MODE_FOLD, PAL>(s, n, smem, cs, query, clusters);
+  std::memset(&ca, 0, sizeof ca);
+  if (!query) {
+    fill_args<T>(s, ca.a, s->cur, s->cur, 0, (int32_t)s->H, (int)n);
+    ca.a.n_strips = 0;
+    ca.a.hb = 0;
+    ca.idx = s->d_idx;
+    ca.pal = static_cast<const T*>(s->d_pal);
+    ca.probes = s->d_probes;
+    ca.first_fire = s->d_first;
+    ca.n_probes = (int32_t)s->probes.size();
+    ca.probe_step = (!s->probes.empty() && probe_due(s, s->step + n)) ? s->step + n : -1;
+    ca.cs = cs;
+    ca.n = (int32_t)n;
+  }
+  const bool react = !(s->g.flags & RD_REACTION_OFF);
+  return rdl::launch_cr(ca, react ? s->fast_mode : rdk::MODE_PRECISE, react, pal, cs, (unsigned)s->B, smem,
+                        s->stream, query, clusters);
 }
 
 cudaError_t cr_dispatch(rd_sim* s, bool pal, int64_t n, size_t smem, int cs, bool query, int* clusters) {
-  if (s->esz == 4)
-    return pal ? launch_cr_mode<float, true>(s, n, smem, cs, query, clusters)
-               : launch_cr_mode<float, false>(s, n, smem, cs, query, clusters);
-  return pal ? launch_cr_mode<double, true>(s, n, smem, cs, query, clusters)
-             : launch_cr_mode<double, false>(s, n, smem, cs, query, clusters);
+  return s->esz == 4 ? launch_cr_t<float>(s, pal, n, smem, cs, query, clusters)
+                     : launch_cr_t<double>(s, pal, n, smem, cs, query, clusters);
 }
 
 // Per-step time models of the two small-grid paths, fitted to configs 1-3 on
