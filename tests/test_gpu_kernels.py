@@ -216,3 +216,24 @@ def test_c_abi_from_plain_c(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     assert "C ABI ok" in out.stdout
+
+
+@pytest.fixture(scope="module")
+def divcheck64(tmp_path_factory):
+    exe = str(tmp_path_factory.mktemp("cuda64") / "divcheck64")
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-o", exe,
+                    os.path.join(HERE, "cuda", "divcheck64.cu")], check=True)
+    return exe
+
+
+@pytest.mark.parametrize("q", ["0.002", "0.5", "1e-12", "0.999"])
+def test_fast_division_f64_matches_ddiv_rn(divcheck64, q):
+    """The inline fp64 fast path (rdk::div_fast_f64) equals __ddiv_rn bitwise
+    wherever its guard passes, on 2^32 seeded reaction operands a = C - q,
+    b = C + q (any finite bit pattern, U[-2, 2], and C within 2^-40 of -q and
+    +q); a tripped guard means a PRECISE replay, never a wrong quotient."""
+    out = subprocess.run([divcheck64, q, str(1 << 32)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    r = json.loads(out.stdout)
+    assert r["tested"] > 3_000_000_000
+    assert r["mismatch_guarded"] == 0, r
