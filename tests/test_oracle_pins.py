@@ -481,3 +481,61 @@ def test_rest_fill_is_stationary():
     assert r.first_fire == [-1] and np.abs(r.u - u).max() < 1e-4
     u32, _ = oracle.rest_fill(phi.astype(np.float32))
     assert u32.dtype == np.float32 and u32[0, 0] == np.float32(oracle.rest_state(float(np.float32(0.054))))
+
+
+# ------------------------------------------------------------ P-6 nullclines
+
+def _u_nullcline_v(u, phi, p=oracle.Params()):
+    """Eq. 1 (P:89-94): du/dt = 0 <=> v = [(u - u^2)(u + q)/(u - q) - phi] / f."""
+    return ((u - u * u) * (u + p.q) / (u - p.q) - phi) / p.f
+
+
+@pytest.mark.parametrize("u", [0.01, 0.0563, 0.2, 0.5, 0.9396])
+def test_reaction_vanishes_on_the_u_nullcline(u):
+    """SURVEY P-6: the oracle's reaction du/dt is zero (to rounding) on the
+    closed-form u-nullcline, and dv/dt = u - v vanishes on v = u."""
+    phi = 0.054
+    v = _u_nullcline_v(u, phi)
+    du, dv = oracle.reaction(u, v, phi)
+    scale = (u + u * u + abs(v) + phi) / oracle.Params().eps
+    assert abs(du) <= 1e-13 * scale
+    assert oracle.reaction(u, u, phi)[1] == 0.0
+
+
+def test_excitability_threshold_between_the_nullcline_crossings():
+    """SURVEY P-6: at v = v* (the rest level) the u-nullcline crosses at the
+    threshold u ~= 0.0563 and the excited branch u ~= 0.9396 (phi = 0.054).
+    A homogeneous medium (no diffusion, so the grid is the ODE) started just
+    below the threshold relaxes to rest; just above it, u jumps to the
+    excited branch (u > 0.5)."""
+    phi = 0.054
+    ustar = oracle.rest_state(phi)
+    # the crossings of the u-nullcline with v = v*: bracket and bisect the
+    # closed form, then check the documented values
+    def cross(lo, hi):
+        f = lambda x: _u_nullcline_v(x, phi) - ustar  # noqa: E731
+        for _ in range(200):
+            m = 0.5 * (lo + hi)
+            if (f(lo) > 0) == (f(m) > 0):
+                lo = m
+            else:
+                hi = m
+        return 0.5 * (lo + hi)
+    th, ex = cross(0.01, 0.3), cross(0.5, 0.999)
+    assert abs(th - 0.0563) < 5e-4 and abs(ex - 0.9396) < 5e-4
+    n = 3
+    phi_p = np.full((n, n), phi)
+    peaks = []
+    for u0 in (th - 0.01, th + 0.01):
+        u = np.full((n, n), u0)
+        v = np.full((n, n), ustar)
+        peak = u0
+        for _ in range(30):
+            r = oracle.run(u, v, phi_p, 100)
+            u, v = r.u, r.v
+            peak = max(peak, float(u.max()))
+        peaks.append(peak)
+    # below: back to rest without crossing the threshold; above: a jump onto
+    # the excited branch (its peak sits below the v = v* crossing because v
+    # rises during the excursion: eps is small, not zero)
+    assert peaks[0] < th and peaks[1] > 0.5
