@@ -2,7 +2,7 @@
 the oracle, bitwise.
 
 Each case draws (from a fixed seed) a dtype, a batch of 1-3 instances with
-ragged shapes, two-level phi maps with obstacles, noisy u/v, stimuli of every
+ragged shapes (one in eight up to 300x400: cr_kernel's palette layout), two-level phi maps with obstacles, noisy u/v, stimuli of every
 kind (disc, rect, half-disc, with and without the phi mask) at random steps,
 latched probes, a timelapse stride, sometimes per-instance Eq.-1 parameters
 (including a non-power-of-two dx, which forces the PRECISE mode), a temporal
@@ -11,6 +11,8 @@ the run into rd_step calls. Fields, probe latches and the timelapse record
 must equal the oracle's exactly; a non-finite fault must stop at the oracle's
 step and cell.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -19,7 +21,7 @@ import paper_1901_06535_b200 as rd
 from rdinputs import noise_plane
 
 pytestmark = pytest.mark.gpu
-N_CASES = 96
+N_CASES = int(os.environ.get("RD_FUZZ_CASES", "96"))  # more seeds on demand
 
 
 def _case(seed):
@@ -27,6 +29,8 @@ def _case(seed):
     dt = np.float32 if g.random() < 0.6 else np.float64
     B = int(g.integers(1, 4))
     H, W = int(g.integers(3, 160)), int(g.integers(3, 260))
+    if g.random() < 0.125:  # large instances: cr_kernel's palette layout in fp64
+        B, H, W = int(g.integers(1, 3)), int(g.integers(200, 301)), int(g.integers(300, 401))
     steps = int(g.integers(1, 90))
     phis, inits, evs, prs, params = [], [], [], [], []
     for b in range(B):
