@@ -4,11 +4,11 @@
 namespace rdl {
 namespace {
 
-template <typename T, bool REACT, int MODE, bool PAL>
-cudaError_t go(const rdk::CrArgs<T>& ca, int cs, unsigned batch, size_t smem, cudaStream_t st, bool query,
-               int* clusters) {
+template <typename T, bool REACT, int MODE, bool PAL, bool PROBE>
+cudaError_t go_p(const rdk::CrArgs<T>& ca, int cs, unsigned batch, size_t smem, cudaStream_t st, bool query,
+                 int* clusters) {
   constexpr int nt = rdk::cr_threads<T>();
-  auto fn = rdk::cr_kernel<T, REACT, MODE, nt, PAL>;
+  auto fn = rdk::cr_kernel<T, REACT, MODE, nt, PAL, PROBE>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
@@ -26,6 +26,16 @@ cudaError_t go(const rdk::CrArgs<T>& ca, int cs, unsigned batch, size_t smem, cu
   cfg.numAttrs = 1;
   if (query) return cudaOccupancyMaxActiveClusters(clusters, fn, &cfg);
   return cudaLaunchKernelEx(&cfg, fn, ca);
+}
+
+// segments with a probe due inside take the variant that evaluates probes in
+// its step loop; the others keep the loop without that code (the latency-bound
+// small bands pay for every instruction on the step's critical path)
+template <typename T, bool REACT, int MODE, bool PAL>
+cudaError_t go(const rdk::CrArgs<T>& ca, int cs, unsigned batch, size_t smem, cudaStream_t st, bool query,
+               int* clusters) {
+  return ca.probe_every ? go_p<T, REACT, MODE, PAL, true>(ca, cs, batch, smem, st, query, clusters)
+                        : go_p<T, REACT, MODE, PAL, false>(ca, cs, batch, smem, st, query, clusters);
 }
 
 template <typename T, bool PAL>

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <numeric>
 #include <tuple>
 #include <cstdarg>
 #include <cstdio>
@@ -439,6 +440,13 @@ cudaError_t launch_cr_t(rd_sim* s, bool pal, int64_t n, size_t smem, int cs, boo
     ca.first_fire = s->d_first;
     ca.n_probes = (int32_t)s->probes.size();
     ca.probe_step = (!s->probes.empty() && probe_due(s, s->step + n)) ? s->step + n : -1;
+    ca.step0 = s->step;
+    int64_t every = 0;  // gcd of the strides of the probes due strictly inside (step, step + n)
+    for (const auto& q : s->probes)
+      if (q.stride > 0 && (s->step + n - 1) / q.stride > s->step / q.stride)
+        every = std::gcd(every, (int64_t)q.stride);
+    ca.probe_every = (int32_t)every;
+    ca.probe_first = every ? (int32_t)(every - s->step % every) : 0;
     ca.cs = cs;
     ca.n = (int32_t)n;
   }
@@ -562,10 +570,16 @@ void palette_add(rd_sim* s, int64_t b, double value) {
   s->pal_dirty = true;
 }
 
-// One cluster-resident launch of n steps. It evaluates the probes due at its
-// last step and needs no global mirror margins (it mirrors from the band), so
+// One cluster-resident launch of n steps. It evaluates the probes due at any
+// of its steps and needs no global mirror margins (it mirrors from the band), so
 // none are refreshed after it: the margins are marked stale and the next
 // consumer that reads them (tb/lp launches) refreshes them first.
+// Whether run_blocks runs the next segment as one cr_kernel launch (which
+// evaluates the due probes itself, so run_range does not cut at them).
+bool cr_runs(const rd_sim* s) {
+  return s->use_cr && (!s->cr_pal || s->pal_ok) && !s->precise_mode && !(s->g.flags & RD_NO_CHECKPOINT);
+}
+
 int launch_cr(rd_sim* s, int64_t n) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (s->profiling) {
@@ -706,8 +720,7 @@ bool probe_due(const rd_sim* s, int64_t step) {
 // small-grid run costs one graph launch per segment instead of two kernel
 // launches per block (the per-launch overhead dominates small batched grids).
 int run_blocks(rd_sim* s, int64_t next, int kmax) {
-  if (s->use_cr && (!s->cr_pal || s->pal_ok) && !s->precise_mode && !(s->g.flags & RD_NO_CHECKPOINT) &&
-      next > s->step) {
+  if (cr_runs(s) && next > s->step) {
     if (int rc = launch_cr(s, next - s->step)) return rc;
     s->step = next;
     return RD_OK;
@@ -807,8 +820,9 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
     int64_t next = end;
     for (const auto& ev : s->events)
       if (ev.at > s->step) next = std::min(next, ev.at);
-    for (const auto& q : s->probes)
-      if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
+    if (!cr_runs(s))  // cr_kernel latches the probes due inside its segment
+      for (const auto& q : s->probes)
+        if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
     if (s->tl_stride > 0) next = std::min(next, (s->step / s->tl_stride + 1) * (int64_t)s->tl_stride);
     if ((rc = run_blocks(s, next, kmax))) return rc;
     if (probe_due(s, s->step) && s->probes_done_at != s->step)
