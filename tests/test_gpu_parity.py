@@ -160,6 +160,29 @@ def test_probes_latch_and_immediate(dtype):
 
 
 @pytest.mark.parametrize("dtype", DT, ids=IDS)
+@pytest.mark.parametrize("splits", [None, [90, 7, 203, 2200]], ids=["one_call", "split"])
+def test_probe_strides_inside_and_at_launch_ends(dtype, splits, kernel):
+    """a6 with strides 30 and 45 in one instance: cr_kernel tests the due steps
+    inside a launch in its step loop (every gcd = 15 steps) and the step that
+    ends a launch in its write-back. rd_step splits end before, on and after
+    due steps. Latched steps and fields equal the oracle's under every kernel."""
+    H, W = 64, 256
+    w = _noise_workload(H, W, dtype, 2500, B=2, n_discs=0)
+    w.init = None
+    w.events = [[({"kind": "rect", "y0": 0, "x0": 0, "y1": H, "x1": 4}, 1.0, 0)],
+                [({"kind": "rect", "y0": 20, "x0": 0, "y1": 44, "x1": 4}, 1.0, 0)]]
+    w.probes = [[((0, 6, H, 8), 0.1, 30), ((0, 10, H, 12), 0.1, 45), ((0, 14, 9, 16), 0.1, 45), ((0, 250, H, 256), 0.1, 30)],
+                [((30, 8, 34, 10), 0.1, 45), ((0, 12, 2, 14), 0.1, 30)]]
+    U, V, fire, _ = gpu_run(w, splits=splits)
+    for b in range(2):
+        r = oracle_run(w, b)
+        assert fire[b] == r.first_fire, (b, fire[b], r.first_fire)
+        assert_bitwise(U[b], r.u, f"u[{b}]")
+        assert_bitwise(V[b], r.v, f"v[{b}]")
+    assert fire[0][0] > 0 and fire[0][1] > 0 and fire[0][0] != fire[0][1] and fire[0][3] == -1
+
+
+@pytest.mark.parametrize("dtype", DT, ids=IDS)
 @pytest.mark.parametrize("tb", [1, 4, 8])
 def test_nonfinite_fault_matches_oracle(dtype, tb, kernel):
     """T5: uniform phi=0.2, noisy u,v, an unmasked u:=1 half-disc -> Euler
