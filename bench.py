@@ -158,6 +158,59 @@ def max_over_ranks(x: float, world: int) -> float:
 
 # ------------------------------------------------------------- our arm
 
+def e2e_pipelined(rd, sim, w, dtype, tb, pu, pv, T, depth, steps, cells):
+    """e2e with `depth` handles of the same workload, each driven by its own
+    host thread through the public API (ctypes releases the GIL; each handle
+    has its own CUDA stream). Every step still copies its inputs in from
+    pinned host memory and its result out, inside the timed region; one job's
+    copies overlap another job's stencil launches (copy engines vs SMs).
+    Timed on the host clock between two device synchronisations."""
+    import torch
+    sims = [sim] + [rd.Sim(None, shape=(1, w.H, w.W), dtype=dtype, tb_depth=tb)
+                    for _ in range(depth - 1)]
+    try:
+        rd.rd_set_stream(sim.h, 0)  # back to the handle's own stream
+        for s in sims[1:]:
+            s.paint_phi(0.054)
+            for shape, val, at in w.events[0]:
+                s.stimulate(shape, val, at)
+            s.write(0, pu, pv)
+            s.step(T)  # warm-up: events consumed, segment graphs captured
+        outs = [(torch.empty(pu.shape, dtype=torch.float32, pin_memory=True).numpy(),
+                 torch.empty(pu.shape, dtype=torch.float32, pin_memory=True).numpy()) for _ in sims]
+        counts = [steps // depth + (1 if k < steps % depth else 0) for k in range(depth)]
+        errors = []
+
+        def job(k):
+            try:
+                for _ in range(counts[k]):
+                    rd.rd_write_fields(sims[k].h, 0, pu, pv)
+                    sims[k].step(T)
+                    rd.rd_read_fields(sims[k].h, 0, *outs[k])
+            except Exception as e:  # surfaced below
+                errors.append(e)
+
+        threads = [threading.Thread(target=job, args=(k,)) for k in range(depth)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        if errors:
+            raise errors[0]
+    finally:
+        for s in sims[1:]:
+            s.close()
+    return {"value": cells * T * steps / secs / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": 2 * cells * 4, "d2h_bytes_per_step": 2 * cells * 4, "steps": steps,
+            "pipeline": depth, "timer": "host clock between device synchronisations",
+            "api": f"{depth} handles, one host thread each: rd_write_fields(host pinned) + rd_step + "
+                   "rd_read_fields(host) every step"}
+
+
 def run_ours(args):
     import torch
     import paper_1901_06535_b200 as rd
@@ -308,6 +361,10 @@ def run_ours(args):
                "api": ("rd_write_fields(host pinned) + rd_step + rd_read_fields(host)" if world == 1 else
                        "per rank: rd_write_fields(host pinned, owned rows) + SlabSim.step (NCCL halos) + "
                        "rd_read_fields(host); bytes per rank, time max over ranks")}
+        if world == 1 and args.e2e_pipeline > 1:
+            serial = e2e
+            e2e = e2e_pipelined(rd, sim, w, dtype, args.tb, pu, pv, T, args.e2e_pipeline, args.e2e_pipeline_steps, cells)
+            e2e["serial"] = {"value": serial["value"], "steps": serial["steps"], "api": serial["api"]}
 
     cpu = None
     if rank == 0 and world == 1 and not strong and not args.no_cpu_baseline:
@@ -405,6 +462,9 @@ def main():
     ap.add_argument("--timesteps", type=int, default=1000, help="time steps per bench step")
     ap.add_argument("--tb", type=int, default=0, help="temporal-blocking depth (0 = auto)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-pipeline", type=int, default=2,
+                    help="handles (host threads) of the pipelined e2e leg at N = 1 (1: serial only)")
+    ap.add_argument("--e2e-pipeline-steps", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--p2p", action="store_true",

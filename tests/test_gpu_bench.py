@@ -23,7 +23,8 @@ def _line(args, timeout=600):
 
 
 def test_bench_line_has_the_contract_keys():
-    d = _line(["--timesteps", "20", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "1"])
+    d = _line(["--timesteps", "20", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "1",
+               "--e2e-pipeline-steps", "3"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
@@ -38,6 +39,7 @@ def test_bench_line_has_the_contract_keys():
     assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] >= 1 and c["sample"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["pipeline"] == 2 and e["steps"] == 3 and e["serial"]["value"] > 0 and e["serial"]["steps"] == 1
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
 
