@@ -5,7 +5,7 @@ nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv,
 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench_default.log
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_reference.log
 python scripts/bench_configs.py > gpurun_out/bench_configs.log 2>&1; echo "configs rc=$?"; cat gpurun_out/bench_configs.log
-CMD="python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 3 --e2e-steps 1 --e2e-pipeline 1 --no-cpu-baseline"
 $CMD > gpurun_out/plain_list.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo "launch list rc=$?"
@@ -15,5 +15,5 @@ ncu --set full --clock-control none --import-source on -k regex:tb_kernel -s 20 
 echo "full rc=$?"
 CMD3="python scripts/bench_configs.py --configs 2 --dtype f32 --repeat 1"
 $CMD3 > gpurun_out/plain_cr.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:cr_kernel -s 20 -c 1 -o gpurun_out/prof_cr $CMD3 > gpurun_out/ncu_cr.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:cr_kernel -s 0 -c 1 -o gpurun_out/prof_cr $CMD3 > gpurun_out/ncu_cr.log 2>&1
 echo "cr rc=$?"
