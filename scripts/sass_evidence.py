@@ -60,7 +60,7 @@ def main():
                     per[fam][mn] += 1
     res = subprocess.run(["cuobjdump", "-res-usage", LIB], capture_output=True, text=True).stdout
     usage = {}
-    for want in ("tb_kernelIfLi4ELi4ELb1ELi4E", "cr_kernelIfLb1ELi4ELi768ELb0E", "cr_kernelIdLb1ELi2ELi768ELb1E",
+    for want in ("tb_kernelIfLi4ELi4ELb1ELi4E", "cr_kernelIfLb1ELi4ELi768ELb0ELb1E", "cr_kernelIdLb1ELi2ELi768ELb1ELb1E",
                  "tb_kernelIdLi4ELi2ELb1ELi2E"):
         m = re.search(r"Function (\S*" + want + r"\S*):\s*\n\s*(REG:\d+.*)", res)
         if m:
