@@ -50,3 +50,24 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "configs[3]" in d["config"]["workload"]
+
+
+def test_bench_two_ranks_under_torchrun():
+    """The driver's N > 1 launch (torchrun, one process per rank) of the
+    weak-scaling line: 16384 rows per rank, row slabs with halo exchange.
+    Both ranks share this box's one GPU, so the exchange runs over gloo
+    (host-staged halos; RD_BENCH_BACKEND) -- a functional check of the
+    N > 1 code path and its JSON line, not a measurement."""
+    env = dict(os.environ, RD_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--timesteps", "8", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
+           "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["steps"] == 3
+    assert "configs[4]" in d["config"]["workload"]
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
