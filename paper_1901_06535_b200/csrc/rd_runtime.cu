@@ -461,17 +461,17 @@ cudaError_t cr_dispatch(rd_sim* s, bool pal, int64_t n, size_t smem, int cs, boo
 }
 
 // Per-step time models of the two small-grid paths, fitted to configs 1-3 on
-// B200 (scripts/bench_configs.py): cr_kernel costs a
-// barrier-and-exchange constant plus its band's cells on one SM; tb_kernel a
-// pipeline-latency floor plus the whole batch spread over the chip. fp64 cr
-// bands are ALU-latency bound (DFMA chains), so large fp64 batches of a few
-// instances stay on tb_kernel, which uses every SM.
+// B200 (scripts/bench_configs.py, same-box runs): cr_kernel
+// costs a per-step sync constant plus its band's cells on one SM; tb_kernel a
+// pipeline-latency floor or, above it, the whole batch spread over the chip.
+// fp64 cr bands are ALU-latency bound (DFMA chains), so large fp64 batches of
+// a few instances stay on tb_kernel, which uses every SM.
 bool cr_beats_tb(const rd_sim* s, int cs) {
   const bool f32 = s->esz == 4;
   const double band = (double)((s->H + cs - 1) / cs) * (double)s->W;
   const double total = (double)s->B * (double)s->H * (double)s->W;
-  const double t_cr = 0.3e-6 + band * (f32 ? 0.29e-9 : 0.64e-9);
-  const double t_tb = (f32 ? 2.9e-6 : 3.5e-6) + total * (f32 ? 1.9e-12 : 4.7e-12);
+  const double t_cr = (f32 ? 0.38e-6 : 0.31e-6) + band * (f32 ? 0.19e-9 : 0.50e-9);
+  const double t_tb = std::max(f32 ? 3.0e-6 : 3.7e-6, total * (f32 ? 7.9e-12 : 11.9e-12));
   return t_cr < t_tb;
 }
 
