@@ -94,10 +94,19 @@ class _DevRows:
         self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
 
 
-def _dev_rows(h, b: int, plane: int, r0: int, r1: int):
+def _dev_rows(h, b: int, plane: int, r0: int, r1: int, cache=None):
+    """Rows [r0, r1) of plane (0 = u, 1 = v) of instance b in the handle's
+    current buffer, as a uint8 CUDA tensor view (cached by device address:
+    the buffers alternate, so a slab reuses two sets of views)."""
     import torch
     ptr, pitch = rd_row_ptr(h, b, plane, r0)
-    return torch.as_tensor(_DevRows(ptr, pitch * (r1 - r0)), device="cuda")
+    key = (ptr, pitch * (r1 - r0))
+    if cache is not None and key in cache:
+        return cache[key]
+    t = torch.as_tensor(_DevRows(ptr, pitch * (r1 - r0)), device="cuda")
+    if cache is not None:
+        cache[key] = t
+    return t
 
 
 class SlabSim:
@@ -179,6 +188,7 @@ class SlabSim:
             rd_stream_wait(self.h, f, self.epoch)
 
     def close(self):
+        self.__dict__.pop("_views", None)  # views of the planes freed below
         if self.h:
             rd_destroy(self.h)
             self.h = None
@@ -210,9 +220,10 @@ class SlabSim:
     def device_tensors(self, b: int):
         """[(peer, [send u, send v], [recv u, recv v])] for the current buffers."""
         out = []
+        cache = self.__dict__.setdefault("_views", {})
         for peer, (s0, s1), (r0, r1) in self.plan:
-            sends = [_dev_rows(self.h, b, p, s0, s1) for p in (0, 1)]
-            recvs = [_dev_rows(self.h, b, p, r0, r1) for p in (0, 1)]
+            sends = [_dev_rows(self.h, b, p, s0, s1, cache) for p in (0, 1)]
+            recvs = [_dev_rows(self.h, b, p, r0, r1, cache) for p in (0, 1)]
             out.append((peer, sends, recvs))
         return out
 
