@@ -180,15 +180,24 @@ def e2e_pipelined(rd, sim, w, dtype, tb, pu, pv, T, depth, steps, cells):
                  torch.empty(pu.shape, dtype=torch.float32, pin_memory=True).numpy()) for _ in sims]
         counts = [steps // depth + (1 if k < steps % depth else 0) for k in range(depth)]
         errors = []
+        # staggered start: job k begins once job k-1's first inputs are on the
+        # device, so the first launch does not wait for every job's upload
+        uploaded = [threading.Event() for _ in range(depth)]
 
         def job(k):
             try:
-                for _ in range(counts[k]):
+                if k:
+                    uploaded[k - 1].wait()
+                for i in range(counts[k]):
                     rd.rd_write_fields(sims[k].h, 0, pu, pv)
+                    if i == 0:
+                        uploaded[k].set()
                     sims[k].step(T)
                     rd.rd_read_fields(sims[k].h, 0, *outs[k])
             except Exception as e:  # surfaced below
                 errors.append(e)
+            finally:
+                uploaded[k].set()
 
         threads = [threading.Thread(target=job, args=(k,)) for k in range(depth)]
         torch.cuda.synchronize()
@@ -464,7 +473,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-pipeline", type=int, default=2,
                     help="handles (host threads) of the pipelined e2e leg at N = 1 (1: serial only)")
-    ap.add_argument("--e2e-pipeline-steps", type=int, default=8)
+    ap.add_argument("--e2e-pipeline-steps", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--p2p", action="store_true",
