@@ -163,7 +163,8 @@ def e2e_pipelined(rd, sim, w, dtype, tb, pu, pv, T, depth, steps, cells):
     host thread through the public API (ctypes releases the GIL; each handle
     has its own CUDA stream). Every step still copies its inputs in from
     pinned host memory and its result out, inside the timed region; one job's
-    copies overlap another job's stencil launches (copy engines vs SMs).
+    copies overlap another job's stencil launches (copy engines vs SMs), and
+    the jobs' stencil launches do not overlap each other (one steps at a time).
     Timed on the host clock between two device synchronisations."""
     import torch
     sims = [sim] + [rd.Sim(None, shape=(1, w.H, w.W), dtype=dtype, tb_depth=tb)
@@ -183,6 +184,10 @@ def e2e_pipelined(rd, sim, w, dtype, tb, pu, pv, T, depth, steps, cells):
         # staggered start: job k begins once job k-1's first inputs are on the
         # device, so the first launch does not wait for every job's upload
         uploaded = [threading.Event() for _ in range(depth)]
+        # one job steps at a time (two concurrent stencil grids would share
+        # the SMs and break tb_kernel's one-wave schedule); uploads and
+        # read-backs of the other jobs proceed meanwhile on the copy engines
+        compute = threading.Lock()
 
         def job(k):
             try:
@@ -192,7 +197,8 @@ def e2e_pipelined(rd, sim, w, dtype, tb, pu, pv, T, depth, steps, cells):
                     rd.rd_write_fields(sims[k].h, 0, pu, pv)
                     if i == 0:
                         uploaded[k].set()
-                    sims[k].step(T)
+                    with compute:
+                        sims[k].step(T)
                     rd.rd_read_fields(sims[k].h, 0, *outs[k])
             except Exception as e:  # surfaced below
                 errors.append(e)
