@@ -330,6 +330,39 @@ def test_probe_latch_semantics():
     assert r.first_fire == [50, -1, 7]
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_probe_max_is_the_rect_maximum(dtype):
+    """a probe reads the maximum of u over [y0,y1)x[x0,x1).
+    Pinned to numpy's max / nanmax (library routines) on a seeded random field,
+    on ragged, single-cell, single-row and full-grid rects; NaN cells never
+    win (R-23)."""
+    rng = np.random.default_rng(11)
+    u = rng.uniform(-1.0, 1.0, (23, 37)).astype(dtype)
+    rects = [(0, 0, 23, 37), (3, 5, 4, 6), (7, 0, 8, 37), (0, 30, 23, 37), (11, 13, 19, 29), (22, 36, 23, 37)]
+    for rect in rects:
+        y0, x0, y1, x1 = rect
+        assert oracle.probe_max(u, rect) == float(u[y0:y1, x0:x1].max())
+    un = u.copy()
+    un[12, 14] = np.nan
+    un[11, 13] = np.nan
+    assert oracle.probe_max(un, (11, 13, 19, 29)) == float(np.nanmax(un[11:19, 13:29]))
+
+
+def test_probe_threshold_is_inclusive():
+    """SPEC.md:243-247 "fired iff max >= threshold": a threshold equal to the
+    rect's maximum after the sampled step fires, the next double above it does
+    not."""
+    rng = np.random.default_rng(5)
+    u0 = rng.uniform(0.0, 0.5, (12, 12))
+    v0 = rng.uniform(0.0, 0.5, (12, 12))
+    phi = np.full((12, 12), 0.054)
+    u1, _ = oracle.step(u0, v0, phi)
+    rect = (2, 3, 9, 10)
+    m = float(u1[2:9, 3:10].max())
+    r = oracle.run(u0, v0, phi, 1, probes=[(rect, m, 1), (rect, np.nextafter(m, np.inf), 1)])
+    assert r.first_fire == [1, -1]
+
+
 def test_rest_state_never_fires():
     """a quiescent medium never reaches the 0.1 threshold; zeros
     relax to the rest state without firing (R-10)."""
