@@ -109,6 +109,19 @@ def test_stimulus_spec_examples():
     assert oracle.stamp(u, u, {"kind": "disc", "cy2": 127, "cx2": 127, "r": 4}) == brute == 52
 
 
+def test_rect_stamp_is_half_open():
+    """A RECT stimulus covers [y0, y1) x [x0, x1), clipped to the grid
+    (rd.h RD_RECT; SPEC rect regions are half-open): the stamped cells equal
+    numpy slicing of the same box, including boxes that cross every edge."""
+    H, W = 17, 23
+    for (y0, x0, y1, x1) in [(3, 4, 9, 11), (0, 0, 1, 1), (-5, -2, 4, 30), (12, 20, 40, 25), (16, 22, 17, 23)]:
+        u = np.zeros((H, W))
+        n = oracle.stamp(u, u, {"kind": "rect", "y0": y0, "x0": x0, "y1": y1, "x1": x1}, 1.0)
+        want = np.zeros((H, W))
+        want[max(y0, 0):max(min(y1, H), 0), max(x0, 0):max(min(x1, W), 0)] = 1.0
+        assert np.array_equal(u, want) and n == int(want.sum())
+
+
 def test_half_disc_and_mask():
     """Half-disc of radius 8 facing +x: brute-force lattice count; the phi mask
     restricts writes to cells whose phi equals mask_phi (R-22)."""
@@ -361,6 +374,19 @@ def test_probe_threshold_is_inclusive():
     m = float(u1[2:9, 3:10].max())
     r = oracle.run(u0, v0, phi, 1, probes=[(rect, m, 1), (rect, np.nextafter(m, np.inf), 1)])
     assert r.first_fire == [1, -1]
+
+
+def test_fault_reports_first_step_and_cell():
+    """S:62 stop at the first non-finite cell, reporting its step and (row,
+    column). Closed form: u = 1e200 at (3, 5) makes C*C overflow, so
+    u' = C + dt*((C - inf)/eps + ...) = -inf after step 1. Each neighbour only
+    receives Du*dt*16*1e200 = 7.2e197 through the Laplacian, finite. So the run
+    stops at step 1 with the fault at row 3, column 5, and u holds that state."""
+    u0 = np.zeros((9, 11))
+    u0[3, 5] = 1e200
+    r = oracle.run(u0, np.zeros((9, 11)), np.full((9, 11), 0.054), 10)
+    assert r.status != 0 and r.fault == (1, 3, 5)
+    assert np.isneginf(r.u[3, 5]) and np.isfinite(np.delete(r.u.ravel(), 3 * 11 + 5)).all()
 
 
 def test_rest_state_never_fires():
