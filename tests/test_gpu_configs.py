@@ -83,6 +83,63 @@ def test_config5_crop_bitwise():
     assert_bitwise(V[0], r.v, "v")
 
 
+@pytest.mark.parametrize("path", ["handle", "slab"])
+def test_config5_full_size_sampled_blocks(path):
+    """configs[4] at its full 65536^2 (120 GB resident, built on the device as
+    `bench.py --scaling strong` builds it), 24 steps. Sampled 16x16 blocks --
+    the four corners, obstacle corners, stimulus centres, seeded interior
+    points -- equal the oracle run on each block's dependency cone, bitwise.
+    After n steps a cell depends only on cells within n of it, so a window
+    n cells wider than the block on every side is exact at the block. Where
+    the window reaches a global edge it stops there, and the real no-flux
+    boundary applies on both sides. The GPU blocks are read straight from the
+    device rows (rd_row_ptr). path "slab" is the launch configuration the
+    strong-scaling bench line times at N = 1 (SlabSim, halo 4, block protocol);
+    "handle" is a plain rd_create handle."""
+    import torch
+    import paper_1901_06535_b200 as rd
+    import oracle
+    from paper_1901_06535_b200.dist import SlabSim, _dev_rows
+    n, S = 24, 16
+    w = config(5, steps=n)
+    H, W = w.H, w.W
+    sim = (rd.Sim(None, shape=(1, H, W), dtype=np.float32) if path == "handle" else
+           SlabSim(W, H, 0, 1, None, dtype=np.float32, halo=4))
+    try:
+        rd.rd_paint_phi(sim.h, -1, None, 0.054)
+        for rect in w.meta["obstacles"]:
+            rd.rd_paint_phi(sim.h, -1, rect, 0.2)
+        sim.fill_noise(seed=1)
+        for s, val, at in w.events[0]:
+            sim.stimulate(s, val, at)
+        sim.step(n)
+        torch.cuda.synchronize()
+        rng = np.random.default_rng(9)
+        corners = [(0, 0), (0, W - S), (H - S, 0), (H - S, W - S)]
+        obst = [(y0 - S // 2, x0 - S // 2) for (y0, x0, _, _) in w.meta["obstacles"][:3]]
+        stim = [(s["cy2"] // 2 - S // 2, s["cx2"] // 2 - S // 2) for s, _, _ in w.events[0][:3]]
+        rand = [(int(rng.integers(0, H - S)), int(rng.integers(0, W - S))) for _ in range(3)]
+        for (by0, bx0) in corners + obst + stim + rand:
+            by0, bx0 = min(max(by0, 0), H - S), min(max(bx0, 0), W - S)
+            by1, bx1 = by0 + S, bx0 + S
+            wy0, wy1, wx0, wx1 = max(0, by0 - n), min(H, by1 + n), max(0, bx0 - n), min(W, bx1 + n)
+            u0, v0 = w.init_planes(0, wy0, wy1 - wy0)
+            phi = w.phi_plane(0, wy0, wy1 - wy0)[:, wx0:wx1].astype(np.float32)
+            ev = []
+            for s, val, at in w.events[0]:
+                t = dict(s)
+                t["cy2"] -= 2 * wy0
+                t["cx2"] -= 2 * wx0
+                ev.append((t, val, at))
+            r = oracle.run(u0[:, wx0:wx1].astype(np.float32), v0[:, wx0:wx1].astype(np.float32), phi, n, events=ev)
+            for plane, ref in ((0, r.u), (1, r.v)):
+                rows = _dev_rows(sim.h, 0, plane, by0, by1).view(torch.float32).view(S, -1)
+                got = rows[:, 8 + bx0:8 + bx1].cpu().numpy()
+                assert_bitwise(got, ref[by0 - wy0:by1 - wy0, bx0 - wx0:bx1 - wx0], f"plane {plane} block ({by0}, {bx0})")
+    finally:
+        sim.close()
+
+
 def test_config5_device_built_crop_bitwise():
     """configs[4] built on the device (rd_paint_phi background + obstacles,
     rd_fill_noise, masked half-discs) on a 2048^2 crop equals the oracle on
