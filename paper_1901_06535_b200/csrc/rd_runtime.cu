@@ -496,7 +496,10 @@ void choose_cr(rd_sim* s, bool forced) {
     return;
   const int64_t V = 16 / (int64_t)s->esz;
   if ((s->W + V - 1) / V > 512) return;  // a thread per column vector (smallest block size)
+  const char* env_cs = getenv("RD_CR_CS");  // measurement override: one cluster size only
+  const int only_cs = env_cs ? atoi(env_cs) : 0;
   for (int cs : {16, 8, 4, 2}) {
+    if (only_cs && cs != only_cs) continue;
     if (s->H < 2 * cs) continue;
     for (bool pal : {false, true}) {
       if (pal && !s->pal_ok) continue;
