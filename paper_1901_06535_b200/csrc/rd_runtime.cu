@@ -7,10 +7,12 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <tuple>
 #include <cstdarg>
@@ -27,6 +29,16 @@
 namespace {
 
 thread_local std::string g_create_error;
+
+// NVTX ranges (SURVEY.md §5 tracing): rd_step calls, their segments, stamps,
+// replays, checkpoints and halo exchanges show up by name on an nsys / ncu
+// timeline; without a tool attached a range is a no-op call.
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range&) = delete;
+  Range& operator=(const Range&) = delete;
+};
 
 struct PendingEvent {
   int32_t b;  // -1 = all
@@ -117,6 +129,7 @@ struct rd_sim {
   unsigned long long* d_fault = nullptr;  // [0] fault key, [1] (as int) precise flag
   int* d_precise = nullptr;
   bool precise_mode = false;
+  bool defer_samples = false;  // replay: probes / timelapse sampled only after the step's fault check
   int* d_flag = nullptr;
   void* d_scratch = nullptr;  // probe max output
   int num_sms = 148;
@@ -161,6 +174,22 @@ int set_err(rd_sim* s, int code, const char* fmt, ...) {
       return set_err((sim), e_ == cudaErrorMemoryAllocation ? RD_ENOMEM : RD_ECUDA, "%s: %s (%s:%d)", \
                      #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
   } while (0)
+
+// Driver entry points through the runtime (no libcuda link), resolved once per
+// process under a lock: handles may be used on several host threads.
+void* driver_entry(const char* name) {
+  static std::mutex mu;
+  static std::map<std::string, void*> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(name);
+  if (it != cache.end()) return it->second;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    fn = nullptr;
+  cache.emplace(name, fn);
+  return fn;
+}
 
 int check_params(const rd_params* p, std::string* why) {
   const double v[6] = {p->eps, p->f, p->q, p->Du, p->dt, p->dx};
@@ -309,7 +338,8 @@ void fill_args(rd_sim* s, rdk::TBArgs<T>& a, int in, int out, int32_t out_lo, in
   a.tm_row0 = (int32_t)s->row_off;
   a.fault_key = s->d_fault;
   a.precise_flag = s->d_precise;
-  a.tl = (s->tl_stride > 0 && (s->step + K) % s->tl_stride == 0) ? origin<T>(s, s->tl) : nullptr;
+  a.tl = (s->tl_stride > 0 && !s->defer_samples && (s->step + K) % s->tl_stride == 0) ? origin<T>(s, s->tl)
+                                                                                       : nullptr;
   a.push_up_u = a.push_up_v = a.push_dn_u = a.push_dn_v = nullptr;
   a.push_stride_up = a.push_stride_dn = 0;
   a.push_rows = 0;
@@ -636,6 +666,7 @@ void shape_bbox(const rdk::ShapeDev& sh, int64_t Hg, int64_t W, int64_t* i0, int
 }
 
 int apply_event(rd_sim* s, const PendingEvent& ev) {
+  Range r_("rd_stimulate.stamp");
   int64_t i0, i1, j0, j1;
   shape_bbox(ev.shape, s->Hg, s->W, &i0, &i1, &j0, &j1);
   // local rows that exist in this handle (owned + readable ghosts)
@@ -645,15 +676,17 @@ int apply_event(rd_sim* s, const PendingEvent& ev) {
   const int32_t b0 = ev.b < 0 ? 0 : ev.b;
   const int32_t nb = ev.b < 0 ? (int32_t)s->B : 1;
   dim3 block(128);
-  dim3 grid((unsigned)((j1 - j0 + 127) / 128), (unsigned)(x1 - x0), (unsigned)nb);
+  // rows beyond gridDim.y's 65535 cap are covered by the kernel's row loop
+  dim3 grid((unsigned)((j1 - j0 + 127) / 128), (unsigned)std::min<int64_t>(x1 - x0, 65535),
+            (unsigned)std::min<int32_t>(nb, 65535));
   if (s->esz == 4)
     rdk::stamp_kernel<float><<<grid, block, 0, s->stream>>>(
         origin<float>(s, s->u[s->cur]), origin<float>(s, s->phi), s->plane_stride, s->pitch, s->grow0, ev.shape,
-        (float)ev.value, (float)ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
+        (float)ev.value, (float)ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0, nb);
   else
     rdk::stamp_kernel<double><<<grid, block, 0, s->stream>>>(
         origin<double>(s, s->u[s->cur]), origin<double>(s, s->phi), s->plane_stride, s->pitch, s->grow0, ev.shape,
-        ev.value, ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0);
+        ev.value, ev.mask_phi, (int32_t)x0, (int32_t)x1, j0, j1, b0, nb);
   RD_CUDA(s, cudaGetLastError());
   s->st.launches++;
   return RD_OK;
@@ -703,6 +736,7 @@ int sync_probes(rd_sim* s) {
 }
 
 int launch_probes(rd_sim* s, int64_t step) {
+  Range r_("rd_probe.latch");
   const int n = (int)s->probes.size();
   if (!n) return RD_OK;
   if (s->esz == 4)
@@ -728,6 +762,7 @@ bool probe_due(const rd_sim* s, int64_t step) {
 // small-grid run costs one graph launch per segment instead of two kernel
 // launches per block (the per-launch overhead dominates small batched grids).
 int run_blocks(rd_sim* s, int64_t next, int kmax) {
+  Range r_("rd_step.segment");
   if (cr_runs(s) && next > s->step) {
     if (int rc = launch_cr(s, next - s->step)) return rc;
     s->step = next;
@@ -833,9 +868,30 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
         if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
     if (s->tl_stride > 0) next = std::min(next, (s->step / s->tl_stride + 1) * (int64_t)s->tl_stride);
     if ((rc = run_blocks(s, next, kmax))) return rc;
-    if (probe_due(s, s->step) && s->probes_done_at != s->step)
+    if (!s->defer_samples && probe_due(s, s->step) && s->probes_done_at != s->step)
       if ((rc = launch_probes(s, s->step))) return rc;
   }
+  return RD_OK;
+}
+
+// Probe latches and timelapse record due after the step just completed (the
+// deferred samples of a PRECISE replay step).
+int sample_step(rd_sim* s) {
+  if (s->tl_stride > 0 && s->step % s->tl_stride == 0) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((s->B * s->H * s->W + 255) / 256,
+                                                                           (int64_t)s->num_sms * 8));
+    if (s->esz == 4)
+      rdk::tl_update_kernel<float><<<grid, 256, 0, s->stream>>>(origin<float>(s, s->u[s->cur]), origin<float>(s, s->tl),
+                                                                 s->plane_stride, s->pitch, (int32_t)s->H,
+                                                                 (int32_t)s->W, (int32_t)s->B);
+    else
+      rdk::tl_update_kernel<double><<<grid, 256, 0, s->stream>>>(
+          origin<double>(s, s->u[s->cur]), origin<double>(s, s->tl), s->plane_stride, s->pitch, (int32_t)s->H,
+          (int32_t)s->W, (int32_t)s->B);
+    RD_CUDA(s, cudaGetLastError());
+    s->st.launches++;
+  }
+  if (probe_due(s, s->step)) return launch_probes(s, s->step);
   return RD_OK;
 }
 
@@ -858,6 +914,7 @@ int reset_fault(rd_sim* s) {
 // Checkpoint = u, v (current buffers), probe latches, timelapse, step,
 // buffer parity and pending events; restore returns to it exactly.
 int save_checkpoint(rd_sim* s) {
+  Range r_("rd_checkpoint");
   if (!s->ck_u) return set_err(s, RD_EINVAL, "handle created with RD_NO_CHECKPOINT");
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
   RD_CUDA(s, cudaMemcpyAsync(s->ck_u, s->u[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
@@ -874,6 +931,7 @@ int save_checkpoint(rd_sim* s) {
 }
 
 int restore_checkpoint(rd_sim* s) {
+  Range r_("rd_restore");
   if (!s->ck_valid) return set_err(s, RD_ERANGE, "no checkpoint to restore");
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
   s->cur = s->ck_cur;
@@ -924,15 +982,8 @@ int alloc_planes(rd_sim* s) {
 // runtime: no libcuda link). Box = one row segment of 32*V columns of the
 // three planes; coordinates are relative to the plane's allocation start.
 int encode_tmaps(rd_sim* s) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return set_err(s, RD_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(driver_entry("cuTensorMapEncodeTiled"));
+  if (!encode) return set_err(s, RD_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const cuuint64_t block = (cuuint64_t)s->B * s->plane_stride * s->esz;
   const cuuint32_t seg = (cuuint32_t)(32 * (16 / s->esz));
   for (int i = 0; i < 2; ++i) {
@@ -971,15 +1022,20 @@ int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
 // div.rn on every input the reaction can produce (exhaustive check of all
 // 2^32 fp32 values of C on the GPU, a few ms; cached per q per process).
 int certify_q(rd_sim* s, double q, bool* ok) {
+  // handles may be created / re-parameterised on several host threads
+  static std::mutex mu;
   static std::vector<std::pair<uint32_t, bool>> cache;
   const float qf = (float)q;
   uint32_t bits;
   std::memcpy(&bits, &qf, 4);
-  for (const auto& c : cache)
-    if (c.first == bits) {
-      *ok = c.second;
-      return RD_OK;
-    }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& c : cache)
+      if (c.first == bits) {
+        *ok = c.second;
+        return RD_OK;
+      }
+  }
   unsigned long long* d = reinterpret_cast<unsigned long long*>(s->d_scratch);
   RD_CUDA(s, cudaMemsetAsync(d, 0, sizeof(unsigned long long), s->stream));
   rdk::divcert_kernel<<<s->num_sms * 8, 256, 0, s->stream>>>(qf, d);
@@ -987,7 +1043,10 @@ int certify_q(rd_sim* s, double q, bool* ok) {
   unsigned long long h = ~0ull;
   RD_CUDA(s, cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s->stream));
   RD_CUDA(s, cudaStreamSynchronize(s->stream));
-  cache.push_back({bits, h == 0});
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    cache.push_back({bits, h == 0});
+  }
   s->div4_mismatches = (int64_t)h;
   *ok = h == 0;
   return RD_OK;
@@ -1188,17 +1247,30 @@ int copy_fields(rd_sim* s, int32_t b, void* uo, void* vo, cudaMemcpyKind kind, b
   return RD_OK;
 }
 
+// The inputs are staged in instance b's owned rows of the other ping-pong
+// buffer (dead between rd_step calls: every launch overwrites them before
+// reading) and checked there; only if both are finite are they copied into
+// the current buffer, so a rejected write leaves the handle untouched.
 int write_fields(rd_sim* s, int32_t b, const void* u, const void* v, cudaMemcpyKind kind) {
   if (int rc = check_b(s, b)) return rc;
-  if (int rc = copy_fields(s, b, const_cast<void*>(u), const_cast<void*>(v), kind, true)) return rc;
-  void* planes[2] = {s->u[s->cur], s->v[s->cur]};
+  if (!u && !v) return RD_OK;
+  const int st = s->cur ^ 1;
+  void* stage[2] = {s->u[st], s->v[st]};
+  void* live[2] = {s->u[s->cur], s->v[s->cur]};
   const void* bufs[2] = {u, v};
   for (int k = 0; k < 2; ++k) {
     if (!bufs[k]) continue;
+    RD_CUDA(s, cudaMemcpy2DAsync(plane_ptr(s, stage[k], b, 0), s->pitch * s->esz, bufs[k], s->W * s->esz,
+                                 s->W * s->esz, s->H, kind, s->stream));
     int bad = 0;
-    if (int rc = check_finite_dev(s, plane_ptr(s, planes[k], b, 0), s->H, &bad)) return rc;
+    if (int rc = check_finite_dev(s, plane_ptr(s, stage[k], b, 0), s->H, &bad)) return rc;
     if (bad) return set_err(s, RD_ENONFINITE, "rd_write_fields: %s contains non-finite values", k ? "v" : "u");
   }
+  for (int k = 0; k < 2; ++k)
+    if (bufs[k])
+      RD_CUDA(s, cudaMemcpy2DAsync(plane_ptr(s, live[k], b, 0), s->pitch * s->esz, plane_ptr(s, stage[k], b, 0),
+                                   s->pitch * s->esz, s->W * s->esz, s->H, cudaMemcpyDeviceToDevice, s->stream));
+  // refresh the mirrored margins of every plane written
   return launch_mirror(s, u ? s->u[s->cur] : s->v[s->cur], (u && v) ? s->v[s->cur] : nullptr, nullptr, s->r_lo,
                        s->r_hi);
 }
@@ -1316,6 +1388,7 @@ int rd_stimulate(rd_sim* s, int32_t b, const rd_shape* shape, double value, int6
 
 int rd_step(rd_sim* s, int64_t n) {
   if (!s) return RD_EINVAL;
+  Range r_("rd_step");
   if (n < 0) return set_err(s, RD_EINVAL, "n must be >= 0");
   if (s->slab && n > s->halo) return set_err(s, RD_ERANGE, "slab handles step at most halo=%lld steps per call", (long long)s->halo);
   if (n == 0) return RD_OK;
@@ -1339,20 +1412,21 @@ int rd_step(rd_sim* s, int64_t n) {
     // step-by-step exact run (results do not depend on the blocking depth).
     if ((rc = restore_checkpoint(s))) return rc;
     key = ~0ull;
+    Range rr_("rd_step.precise_replay");
     s->precise_mode = true;
+    s->defer_samples = true;
     s->st.replays++;
     while (s->step < step0 + n) {
-      if ((rc = run_range(s, s->step + 1, 1))) {
-        s->precise_mode = false;
-        return rc;
-      }
-      if ((rc = read_fault(s, &key, nullptr))) {
-        s->precise_mode = false;
-        return rc;
-      }
+      // the step without its probe latch and timelapse record; those follow
+      // only once the step is known to be finite (the oracle stops before
+      // sampling a failing step, oracle_body.h orc_run)
+      if ((rc = run_range(s, s->step + 1, 1)) || (rc = read_fault(s, &key, nullptr))) break;
       if (key != ~0ull) break;
+      if ((rc = sample_step(s))) break;
     }
     s->precise_mode = false;
+    s->defer_samples = false;
+    if (rc) return rc;
     if (key == ~0ull) return RD_OK;
   }
   const unsigned long long W = (unsigned long long)s->W, Hg = (unsigned long long)s->Hg;
@@ -1368,6 +1442,7 @@ int rd_step(rd_sim* s, int64_t n) {
 
 int rd_step_unchecked(rd_sim* s, int64_t n) {
   if (!s) return RD_EINVAL;
+  Range r_("rd_step_unchecked");
   if (n < 0) return set_err(s, RD_EINVAL, "n must be >= 0");
   if (s->slab && n > s->halo) return set_err(s, RD_ERANGE, "slab handles step at most halo=%lld steps per call", (long long)s->halo);
   if (n == 0) return RD_OK;
@@ -1532,15 +1607,8 @@ int rd_push_ghosts(rd_sim* s) {
 // reached through the runtime's entry-point query: no libcuda link).
 int rd_stream_signal(rd_sim* s, void* flag, uint32_t value) {
   if (!s || !flag) return RD_EINVAL;
-  static PFN_cuStreamWriteValue32_v11070 fn = nullptr;
-  if (!fn) {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !f)
-      return set_err(s, RD_ECUDA, "cuStreamWriteValue32 entry point unavailable");
-    fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
-  }
+  auto fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(driver_entry("cuStreamWriteValue32"));
+  if (!fn) return set_err(s, RD_ECUDA, "cuStreamWriteValue32 entry point unavailable");
   if (fn(reinterpret_cast<CUstream>(s->stream), reinterpret_cast<CUdeviceptr>(flag), value, 0) != CUDA_SUCCESS)
     return set_err(s, RD_ECUDA, "cuStreamWriteValue32 failed");
   return RD_OK;
@@ -1548,15 +1616,8 @@ int rd_stream_signal(rd_sim* s, void* flag, uint32_t value) {
 
 int rd_stream_wait(rd_sim* s, void* flag, uint32_t value) {
   if (!s || !flag) return RD_EINVAL;
-  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
-  if (!fn) {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !f)
-      return set_err(s, RD_ECUDA, "cuStreamWaitValue32 entry point unavailable");
-    fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(f);
-  }
+  auto fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(driver_entry("cuStreamWaitValue32"));
+  if (!fn) return set_err(s, RD_ECUDA, "cuStreamWaitValue32 entry point unavailable");
   if (fn(reinterpret_cast<CUstream>(s->stream), reinterpret_cast<CUdeviceptr>(flag), value,
          CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
     return set_err(s, RD_ECUDA, "cuStreamWaitValue32 failed");
