@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define RD_ABI_VERSION 1
+#define RD_ABI_VERSION 2
 
 typedef struct rd_sim rd_sim; /* opaque handle */
 
@@ -52,6 +52,7 @@ enum {
   RD_ERANGE = -3,      /* probe rect empty/outside the grid, at_step < current step, instance out of range */
   RD_ENONFINITE = -4,  /* non-finite input, or produced during rd_step; see rd_last_error / rd_get_fault */
   RD_ECUDA = -5,       /* CUDA runtime error (message has the CUDA error string) */
+  RD_ENCCL = -6,       /* NCCL missing (dlopen libnccl.so.2) or an NCCL call failed (rd_create_dist) */
   RD_ENOMEM = -7       /* device or host allocation failed */
 };
 
@@ -138,6 +139,22 @@ typedef struct {
                               1 lp_kernel (level-parallel), 2 cr_kernel (cluster-resident, a8) */
 } rd_stats;
 
+/* Where a handle's rows sit (rd_get_geometry). For rd_create / rd_create_device
+ * handles row0 = 0, height = height_global, rank = 0, world = 1. */
+enum { RD_TRANSPORT_NONE = 0, RD_TRANSPORT_P2P = 1, RD_TRANSPORT_NCCL = 2, RD_TRANSPORT_LOCAL = 3 };
+typedef struct {
+  int64_t width, height;  /* columns; rows this handle owns */
+  int64_t height_global;  /* rows of the whole grid */
+  int64_t row0;           /* global row of owned row 0 */
+  int64_t pitch;          /* elements between rows in device memory (rd_field_ptr) */
+  int64_t phi_rows_lo, phi_rows_hi; /* local rows [lo, hi) a create call's phi buffer covers */
+  int64_t exchanges;      /* halo exchanges performed (dist handles) */
+  int32_t batch, dtype, halo, tb_depth;
+  int32_t rank, world;    /* dist handles: this rank of world; else 0 of 1 */
+  int32_t transport;      /* RD_TRANSPORT_*: how a dist handle's halos travel */
+  int32_t pad;
+} rd_geometry;
+
 /* ---- lifecycle ---- */
 
 /* Table 1 defaults: eps=0.0243, f=1.4, q=0.002, Du=0.45, dt=0.001, dx=0.25. */
@@ -149,8 +166,81 @@ void rd_params_default(rd_params* p);
  * Errors: RD_EINVAL, RD_EPARAM, RD_ENONFINITE (phi), RD_ENOMEM, RD_ECUDA. */
 int rd_create(const rd_grid* grid, const rd_params* params, const void* phi_map, struct rd_sim** out);
 
-/* Release all device memory and the stream (if owned). NULL is a no-op. */
+/* Release all device memory and the stream (if owned). NULL is a no-op.
+ * Collective for rd_create_dist handles (every rank destroys its handle; no
+ * rank frees its planes while a neighbour may still reach them). A caller
+ * arena (rd_create_device) is not freed. */
 int rd_destroy(struct rd_sim* sim);
+
+/* ---- PyTorch (caller-owned) device memory: SURVEY.md §8(b) rd_create_device ----
+ * The planes live in ONE caller allocation (e.g. a torch uint8 CUDA tensor of
+ * rd_arena_bytes bytes, 256-byte aligned) that the handle lays out itself:
+ * u ping-pong, v ping-pong, phi and the checkpoint, each [batch][rows][pitch]
+ * with mirrored ghost margins -- the no-flux boundary and tb_kernel's single
+ * 4-D tensor map per row need that layout, so dense H x W
+ * tensors cannot be adopted as they are. rd_field_ptr gives each plane's
+ * (row 0, column 0) and pitch, for zero-copy strided views.
+ *   rd_arena_bytes    bytes the grid needs (no device work).
+ *   rd_create_device  as rd_create, with the caller's arena (kept alive by the
+ *                     caller until rd_destroy) and phi_dev a DEVICE map
+ *                     [batch][height][width] of dtype (or NULL = 0).
+ *   rd_field_ptr      instance b's current u (plane 0), v (1) or phi (2):
+ *                     device pointer of cell (0, 0), row pitch in elements.
+ *                     Valid until the next rd_step (u, v ping-pong).
+ * Errors: RD_EINVAL (NULL / misaligned / too small arena, bad plane),
+ * RD_ERANGE (b), plus those of rd_create. */
+int rd_arena_bytes(const rd_grid* grid, size_t* bytes);
+int rd_create_device(const rd_grid* grid, const rd_params* params, void* arena, size_t arena_bytes,
+                     const void* phi_dev, struct rd_sim** out);
+int rd_field_ptr(struct rd_sim* sim, int32_t b, int32_t plane, void** ptr, int64_t* pitch_elems);
+int rd_get_geometry(const struct rd_sim* sim, rd_geometry* out);
+
+/* ---- multi-GPU row slabs run by the library ----
+ * BASELINE.json north_star: "a row-slab domain decomposition across the 8
+ * GPUs of one box, with halo exchange by NCCL send/recv or CUDA P2P over
+ * NVLink overlapped with interior compute" (the paper itself runs on one
+ * tablet). One handle per rank: one process per GPU, or
+ * one host thread per rank of one process.
+ *   rd_dist_unique_id  a rendezvous id for ranks in several processes (an
+ *                      NCCL unique id; make it on one rank and broadcast the
+ *                      128 bytes, e.g. with torch.distributed). RD_ENCCL if
+ *                      libnccl.so.2 cannot be loaded.
+ *   rd_dist_local_id   a rendezvous id for ranks that are host threads of
+ *                      THIS process (no NCCL; ranks may share a device, e.g.
+ *                      to test on one GPU; distinct devices need peer access).
+ *   rd_create_dist     rank `rank` of `world` (collective: every rank calls it
+ *                      with the same global grid, params and id; returns when
+ *                      all have joined). The rank owns global rows [row0,
+ *                      row0 + rows): rows = H/G, the first H % G ranks one
+ *                      more (rd_get_geometry). phi_rows: HOST
+ *                      [batch][rows][width] of the OWNED rows (NULL = 0; the
+ *                      ghost rows come from the neighbours). halo = the
+ *                      temporal-blocking depth (grid->tb_depth, 0 = 4); every
+ *                      slab needs rows >= halo.
+ * On a dist handle, rd_step(n) runs the whole super-step inside the library:
+ * a checkpoint; blocks of <= halo steps, each with its halo exchange (u and v
+ * send rows straight into the neighbours' ghost rows by copy-engine
+ * cudaMemcpyAsync over CUDA IPC / peer mappings, ordered by stream-ordered
+ * counters, overlapped with the interior rows; RD_DIST_TRANSPORT=nccl or a
+ * failed peer mapping selects grouped ncclSend/ncclRecv instead); one fault /
+ * guard flag OR over the ranks (ncclAllReduce); on a fault every rank replays
+ * step by step and stops at the first failing step, reporting the global first
+ * cell. Results are bitwise those of one rd_create handle of the whole grid.
+ * Collective calls (every rank, same arguments): rd_create_dist, rd_step,
+ * rd_stimulate, rd_probe_latch, rd_timelapse, rd_set_params, rd_probe (global
+ * max), rd_probe_result (global first firing), rd_destroy. Stimuli, probes,
+ * timelapse and parameters decide the launch sequence, so rd_step checks a
+ * digest of them on all ranks (RD_EINVAL if they differ). Local calls:
+ * rd_write_fields / rd_read_fields (owned rows [rows][width]), rd_paint_phi,
+ * rd_fill_noise, rd_init_rest (global coordinates). The low-level slab calls
+ * (rd_step_begin/finish, rd_step_unchecked, rd_checkpoint/restore,
+ * rd_push_ghosts, rd_set_peer) are refused (RD_EINVAL).
+ * Errors: RD_EINVAL (arguments, unknown local id, slab thinner than the
+ * halo), RD_ENCCL, RD_ECUDA, RD_ENOMEM, RD_ENONFINITE (phi). */
+int rd_dist_unique_id(uint8_t id[128]);
+int rd_dist_local_id(uint8_t id[128]);
+int rd_create_dist(const rd_grid* global, const rd_params* params, const void* phi_rows, int32_t rank,
+                   int32_t world, const uint8_t id[128], struct rd_sim** out);
 
 /* Use an external CUDA stream (cudaStream_t, e.g. torch's current stream)
  * for all subsequent work; NULL reverts to the handle's own (non-blocking)

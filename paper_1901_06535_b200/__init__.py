@@ -16,13 +16,14 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import (RD_DISC, RD_ENONFINITE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_CHECKPOINT,  # noqa: F401
-                   RD_NO_GRAPH, RD_OK, RD_REACTION_OFF, RD_RECT, RD_SHAPE_MASK_PHI, load)
+from ._lib import (RD_DISC, RD_ECUDA, RD_EINVAL, RD_ENCCL, RD_ENOMEM, RD_ENONFINITE, RD_EPARAM, RD_ERANGE, RD_F32, RD_F64, RD_HALF_DISC, RD_NO_CHECKPOINT,  # noqa: F401
+                   RD_NO_GRAPH, RD_OK, RD_REACTION_OFF, RD_RECT, RD_SHAPE_MASK_PHI, TRANSPORTS, load)
 
 __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab", "rd_destroy", "rd_stimulate",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
            "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_step_begin", "rd_step_finish", "RD_BLOCK_PUSH", "rd_plane_origins", "rd_set_peer", "rd_push_ghosts", "rd_flag_ptr", "rd_ipc_export", "rd_ipc_map", "rd_stream_signal", "rd_stream_wait", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
-           "rd_reset_stats", "rd_last_error", "load"]
+           "rd_reset_stats", "rd_last_error", "load", "rd_get_geometry", "rd_arena_bytes", "rd_create_device",
+           "rd_field_ptr", "rd_dist_unique_id", "rd_dist_local_id", "rd_create_dist"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
 _DT = {np.dtype(np.float32): RD_F32, np.dtype(np.float64): RD_F64}
@@ -44,8 +45,48 @@ def _check(rc: int, handle=None, create: bool = False):
 def _ptr(a: np.ndarray | None):
     if a is None:
         return None
-    assert a.flags.c_contiguous
+    if not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
+        raise ValueError("host buffers must be C-contiguous numpy arrays")
     return a.ctypes.data_as(C.c_void_p)
+
+
+_GEOM = {}  # handle address -> rd_get_geometry (dropped by rd_destroy)
+
+
+def _geom(h) -> dict:
+    key = getattr(h, "value", h)
+    g = _GEOM.get(key)
+    if g is None:
+        g = _GEOM[key] = rd_get_geometry(h)
+    return g
+
+
+def _host(a: np.ndarray | None, h, rows: int | None = None, what: str = "buffer", writable: bool = False):
+    """Validate a host buffer the C side reads or writes as rows x width
+    elements of the handle's dtype (owned rows by default): the C side copies
+    exactly that many bytes, so a short or mistyped array must not get
+    through."""
+    if a is None:
+        return None
+    g = _geom(h)
+    dt = np.dtype(np.float32 if g["dtype"] == RD_F32 else np.float64)
+    n = (g["height"] if rows is None else rows) * g["width"]
+    if not isinstance(a, np.ndarray):
+        raise ValueError(f"{what}: expected a numpy array")
+    if a.dtype != dt:
+        raise ValueError(f"{what}: dtype {a.dtype} does not match the handle's {dt}")
+    if a.size != n:
+        raise ValueError(f"{what}: {a.size} elements, expected {n} ({n // g['width']} rows x {g['width']})")
+    if not a.flags.c_contiguous:
+        raise ValueError(f"{what}: must be C-contiguous")
+    if writable and not a.flags.writeable:
+        raise ValueError(f"{what}: must be writable")
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check_map(phi, dt, n: int, what: str):
+    if phi is not None and phi.size != n:
+        raise ValueError(f"{what}: {phi.size} elements, expected {n}")
 
 
 def _shape(s: dict) -> _lib.rd_shape:
@@ -74,7 +115,7 @@ def rd_create(width: int, height: int, phi_map: np.ndarray | None, *, batch: int
     the host, or None for phi = 0 (paint it with rd_paint_phi)."""
     dt = np.dtype(dtype)
     phi = None if phi_map is None else np.ascontiguousarray(phi_map, dtype=dt)
-    assert phi is None or phi.size == batch * height * width
+    _check_map(phi, dt, batch * height * width, "phi_map")
     g = _lib.rd_grid(width, height, batch, _DT[dt], tb_depth, flags, pitch)
     p = params or rd_params_default()
     h = C.c_void_p()
@@ -86,6 +127,8 @@ def rd_create_slab(width: int, height: int, phi_slab: np.ndarray, row0: int, hei
                    batch: int = 1, dtype=np.float32, tb_depth: int = 0, flags: int = 0, params=None):
     dt = np.dtype(dtype)
     phi = None if phi_slab is None else np.ascontiguousarray(phi_slab, dtype=dt)
+    lo, hi = max(0, row0 - halo), min(height_global, row0 + height + halo)
+    _check_map(phi, dt, batch * (hi - lo) * width, "phi_slab (owned + ghost rows)")
     g = _lib.rd_grid(width, height, batch, _DT[dt], tb_depth, flags, 0)
     p = params or rd_params_default()
     h = C.c_void_p()
@@ -95,7 +138,80 @@ def rd_create_slab(width: int, height: int, phi_slab: np.ndarray, row0: int, hei
 
 
 def rd_destroy(h) -> None:
+    _GEOM.pop(getattr(h, "value", h), None)
     _check(load().rd_destroy(h), h)
+
+
+def rd_get_geometry(h) -> dict:
+    """Where the handle's rows sit: width, height (owned rows), height_global,
+    row0, pitch, batch, dtype, halo, tb_depth, rank, world, transport."""
+    g = _lib.rd_geometry()
+    _check(load().rd_get_geometry(h, C.byref(g)), h)
+    d = {k: getattr(g, k) for k, _ in g._fields_ if k != "pad"}
+    d["transport"] = TRANSPORTS.get(d["transport"], d["transport"])
+    return d
+
+
+def rd_arena_bytes(width: int, height: int, *, batch: int = 1, dtype=np.float32, pitch: int = 0) -> int:
+    g = _lib.rd_grid(width, height, batch, _DT[np.dtype(dtype)], 0, 0, pitch)
+    n = C.c_size_t()
+    _check(load().rd_arena_bytes(C.byref(g), C.byref(n)), create=True)
+    return n.value
+
+
+def rd_create_device(width: int, height: int, arena_ptr: int, arena_bytes: int, phi_ptr: int | None, *,
+                     batch: int = 1, dtype=np.float32, tb_depth: int = 0, flags: int = 0, params=None, pitch: int = 0):
+    """rd_create over a caller-owned DEVICE arena (e.g. a torch uint8 CUDA
+    tensor of rd_arena_bytes bytes): phi_ptr is a device map [batch][H][W]
+    (or None). The caller keeps the arena alive until rd_destroy."""
+    g = _lib.rd_grid(width, height, batch, _DT[np.dtype(dtype)], tb_depth, flags, pitch)
+    p = params or rd_params_default()
+    h = C.c_void_p()
+    _check(load().rd_create_device(C.byref(g), C.byref(p), C.c_void_p(arena_ptr), int(arena_bytes),
+                                   C.c_void_p(phi_ptr) if phi_ptr else None, C.byref(h)), create=True)
+    return h
+
+
+def rd_field_ptr(h, b: int, plane: int) -> tuple[int, int]:
+    """(device pointer of cell (0, 0), row pitch in elements) of instance b's
+    current u (0), v (1) or phi (2); valid until the next rd_step."""
+    p, pitch = C.c_void_p(), C.c_int64()
+    _check(load().rd_field_ptr(h, int(b), int(plane), C.byref(p), C.byref(pitch)), h)
+    return p.value, pitch.value
+
+
+def rd_dist_unique_id() -> bytes:
+    """128-byte rendezvous id for ranks in several processes (NCCL unique id)."""
+    buf = C.create_string_buffer(128)
+    _check(load().rd_dist_unique_id(buf), create=True)
+    return buf.raw
+
+
+def rd_dist_local_id() -> bytes:
+    """128-byte rendezvous id for ranks that are host threads of this process."""
+    buf = C.create_string_buffer(128)
+    _check(load().rd_dist_local_id(buf), create=True)
+    return buf.raw
+
+
+def rd_create_dist(width: int, height_global: int, phi_rows: np.ndarray | None, rank: int, world: int, uid: bytes, *,
+                   batch: int = 1, dtype=np.float32, tb_depth: int = 0, flags: int = 0, params=None):
+    """rd_create_dist (collective): rank's row slab of the global grid.
+    phi_rows: host [batch][rows][width] of the OWNED rows (see slab_rows), or
+    None for phi = 0."""
+    dt = np.dtype(dtype)
+    phi = None if phi_rows is None else np.ascontiguousarray(phi_rows, dtype=dt)
+    base, extra = divmod(height_global, world)
+    rows = base + (1 if rank < extra else 0)
+    _check_map(phi, dt, batch * rows * width, "phi_rows (owned rows)")
+    if len(uid) != 128:
+        raise ValueError("uid must be the 128 bytes of rd_dist_unique_id / rd_dist_local_id")
+    g = _lib.rd_grid(width, height_global, batch, _DT[dt], tb_depth, flags, 0)
+    p = params or rd_params_default()
+    h = C.c_void_p()
+    _check(load().rd_create_dist(C.byref(g), C.byref(p), _ptr(phi), int(rank), int(world),
+                                 C.create_string_buffer(uid, 128), C.byref(h)), create=True)
+    return h
 
 
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream as an explicit handle
@@ -224,11 +340,12 @@ def rd_get_fault(h) -> tuple:
 
 
 def rd_read_fields(h, b: int, u_out: np.ndarray | None, v_out: np.ndarray | None) -> None:
-    _check(load().rd_read_fields(h, b, _ptr(u_out), _ptr(v_out)), h)
+    _check(load().rd_read_fields(h, b, _host(u_out, h, what="u_out", writable=True),
+                                 _host(v_out, h, what="v_out", writable=True)), h)
 
 
 def rd_write_fields(h, b: int, u: np.ndarray | None, v: np.ndarray | None) -> None:
-    _check(load().rd_write_fields(h, b, _ptr(u), _ptr(v)), h)
+    _check(load().rd_write_fields(h, b, _host(u, h, what="u"), _host(v, h, what="v")), h)
 
 
 def rd_read_fields_device(h, b: int, u_ptr: int | None, v_ptr: int | None) -> None:
@@ -283,7 +400,7 @@ def rd_timelapse(h, stride: int) -> None:
 
 
 def rd_read_timelapse(h, b: int, out: np.ndarray) -> None:
-    _check(load().rd_read_timelapse(h, b, _ptr(out)), h)
+    _check(load().rd_read_timelapse(h, b, _host(out, h, what="max_u_out", writable=True)), h)
 
 
 def rd_row_ptr(h, b: int, plane: int, row: int) -> tuple[int, int]:

@@ -2,22 +2,30 @@
 
 No JIT cache, no torch extension machinery: a plain shared library with the
 C ABI of include/rd.h, built for `-gencode arch=compute_100a,code=sm_100a`.
+Object files are kept under build/ (git-ignored) and rebuilt only when their
+source or a header they include changed.
 """
 from __future__ import annotations
 
-import glob
 import os
 import subprocess
-import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librd.so")
+OBJDIR = os.path.join(HERE, "build")
+CSRC = os.path.join(HERE, "csrc")
+RD_H = os.path.join(ROOT, "include", "rd.h")
+KERNELS = [os.path.join(CSRC, f) for f in ("rd_kernels.cuh", "rd_launch.h")]
 # the runtime and the kernel-instantiation units (rd_launch.h), compiled in
-# parallel and linked into one shared library
-SOURCES = [os.path.join(HERE, "csrc", f) for f in
-           ("rd_runtime.cu", "rd_launch_tb_f32.cu", "rd_launch_tb_f64.cu", "rd_launch_cr.cu")]
-DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*")) + [os.path.join(ROOT, "include", "rd.h")])
+# parallel and linked into one shared library: source -> headers it includes
+UNITS = {
+    "rd_runtime.cu": KERNELS + [RD_H, os.path.join(CSRC, "rd_dist.cuh")],
+    "rd_launch_tb_f32.cu": KERNELS + [os.path.join(CSRC, "rd_launch_tb.cuh")],
+    "rd_launch_tb_f64.cu": KERNELS + [os.path.join(CSRC, "rd_launch_tb.cuh")],
+    "rd_launch_cr.cu": KERNELS,
+}
+SOURCES = [os.path.join(CSRC, f) for f in UNITS]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,24 +44,34 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def _mtime(p: str) -> float:
+    return os.path.getmtime(p) if os.path.exists(p) else -1.0
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    newest = max(os.path.getmtime(p) for p in DEPS)
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
-    with tempfile.TemporaryDirectory() as tmp:
-        objs, procs = [], []
-        for src in SOURCES:
-            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+    os.makedirs(OBJDIR, exist_ok=True)
+    objs, procs = [], []
+    for name, deps in UNITS.items():
+        src = os.path.join(CSRC, name)
+        obj = os.path.join(OBJDIR, name + ".o")
+        objs.append(obj)
+        newest = max(_mtime(p) for p in [src, *deps, __file__])
+        if force or _mtime(obj) < newest:
             cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
-            procs.append((subprocess.Popen(cmd), cmd))
-            objs.append(obj)
-        for p, cmd in procs:
-            if p.wait() != 0:
-                raise subprocess.CalledProcessError(p.returncode, cmd)
+            procs.append((subprocess.Popen(cmd), cmd, obj))
+    failed = None
+    for p, cmd, obj in procs:
+        if p.wait() != 0:
+            if os.path.exists(obj):
+                os.remove(obj)
+            failed = failed or subprocess.CalledProcessError(p.returncode, cmd)
+    if failed:
+        raise failed
+    if procs or force or _mtime(LIB) < max(_mtime(o) for o in objs):
         subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
-                        "-lcudart"], check=True)
+                        "-lcudart", "-ldl"], check=True)
     return LIB
 
 

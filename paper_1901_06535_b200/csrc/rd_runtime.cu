@@ -10,6 +10,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -55,6 +56,8 @@ struct LatchedProbe {
   int32_t stride;
 };
 
+struct DistState;  // rd_dist.cuh
+
 }  // namespace
 
 struct rd_sim {
@@ -63,6 +66,8 @@ struct rd_sim {
   CUtensorMap tmap[2];
   void* arena = nullptr;  // the plane allocation (u, v, phi, checkpoint, push flags)
   size_t arena_bytes = 0;
+  bool own_arena = true;     // false: caller-owned (rd_create_device)
+  DistState* dist = nullptr;  // rd_create_dist handles (rd_dist.cuh)
   rd_grid g{};
   rd_params p{};
   size_t esz = 4;
@@ -189,6 +194,20 @@ void* driver_entry(const char* name) {
     fn = nullptr;
   cache.emplace(name, fn);
   return fn;
+}
+
+// rd_dist.cuh (dist handles: rd_create_dist)
+int dist_step(rd_sim* s, int64_t n);
+void dist_destroy(rd_sim* s);
+int dist_allmax(rd_sim* s, std::vector<uint64_t>& v);
+int dist_probe_result(rd_sim* s, int64_t local, int64_t* out);
+uint64_t dbl_key(double x);
+double key_dbl(uint64_t k);
+void dist_geometry(const rd_sim* s, rd_geometry* out);
+
+int not_dist(rd_sim* s, const char* what) {
+  if (s->dist) return set_err(s, RD_EINVAL, "%s: not for rd_create_dist handles (the library runs their protocol)", what);
+  return RD_OK;
 }
 
 int check_params(const rd_params* p, std::string* why) {
@@ -954,13 +973,23 @@ int restore_checkpoint(rd_sim* s) {
 // a stride of 3 blocks and u1, v1, phi at a stride of 2, so one tensor map per
 // input buffer (dims col, row, instance, plane) lands a row's u, v and phi
 // segments with one TMA (tb_kernel). The checkpoint fills the two gaps.
-int alloc_planes(rd_sim* s) {
+size_t arena_size(const rd_sim* s) { return 7 * (size_t)s->B * s->plane_stride * s->esz + 256; }
+
+int alloc_planes(rd_sim* s, void* ext, size_t ext_bytes) {
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
   // + 256 bytes: the peer-push flag words (rd_flag_ptr), so one IPC handle
   // of the arena maps planes and flags
-  RD_CUDA(s, cudaMalloc(&s->arena, 7 * bytes + 256));
-  RD_CUDA(s, cudaMemsetAsync(s->arena, 0, 7 * bytes + 256, s->stream));
-  s->arena_bytes = 7 * bytes + 256;
+  if (ext) {
+    if (ext_bytes < arena_size(s) || reinterpret_cast<uintptr_t>(ext) % 256)
+      return set_err(s, RD_EINVAL, "caller arena must be 256-byte aligned and >= %zu bytes (rd_arena_bytes)",
+                     arena_size(s));
+    s->arena = ext;
+    s->own_arena = false;
+  } else {
+    RD_CUDA(s, cudaMalloc(&s->arena, arena_size(s)));
+  }
+  RD_CUDA(s, cudaMemsetAsync(s->arena, 0, arena_size(s), s->stream));
+  s->arena_bytes = arena_size(s);
   char* base = static_cast<char*>(s->arena);
   s->u[0] = base;
   s->u[1] = base + 2 * bytes;
@@ -1100,8 +1129,12 @@ char* plane_ptr(rd_sim* s, void* plane, int64_t b, int64_t local_row) {
          ((size_t)b * s->plane_stride + (size_t)(local_row + s->row_off) * s->pitch + (size_t)s->col_off) * s->esz;
 }
 
+// Shared by rd_create / rd_create_slab / rd_create_device / rd_create_dist.
+// phi_kind: cudaMemcpyHostToDevice (host map) or DeviceToDevice (caller's
+// device map); ext_arena: caller-owned plane allocation (or NULL).
 int create_common(const rd_grid* grid, const rd_params* params, const void* phi_host, int64_t row0,
-                  int64_t Hg, int32_t halo, bool slab, rd_sim** out) {
+                  int64_t Hg, int32_t halo, bool slab, rd_sim** out, void* ext_arena, size_t ext_bytes,
+                  cudaMemcpyKind phi_kind = cudaMemcpyHostToDevice) {
   if (!out) return set_err(nullptr, RD_EINVAL, "out is NULL");
   *out = nullptr;
   if (!grid || !params) return set_err(nullptr, RD_EINVAL, "grid and params are required");
@@ -1169,7 +1202,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
       cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (s->num_sms < 1) s->num_sms = 148;
   }
-  if (int rc = alloc_planes(s)) return fail(rc);
+  if (int rc = alloc_planes(s, ext_arena, ext_bytes)) return fail(rc);
   if (int rc = encode_tmaps(s)) return fail(rc);
   if (int rc = choose_mode(s)) return fail(rc);
   // phi rows present in the host buffer: local [lo, hi)
@@ -1178,7 +1211,7 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
   for (int64_t b = 0; b < s->B && phi_host; ++b) {
     const char* src = (const char*)phi_host + (size_t)b * (hi - lo) * s->W * s->esz;
     cudaError_t e = cudaMemcpy2DAsync(plane_ptr(s, s->phi, b, lo), s->pitch * s->esz, src, s->W * s->esz,
-                                      s->W * s->esz, hi - lo, cudaMemcpyHostToDevice, s->stream);
+                                      s->W * s->esz, hi - lo, phi_kind, s->stream);
     if (e != cudaSuccess) {
       s->err = std::string("phi upload: ") + cudaGetErrorString(e);
       return fail(RD_ECUDA);
@@ -1201,7 +1234,16 @@ int create_common(const rd_grid* grid, const rd_params* params, const void* phi_
       continue;
     }
     std::vector<double> vals((size_t)(s->H * s->W));
+    std::vector<char> staged;
     const char* src = (const char*)phi_host + (size_t)b * s->H * s->W * s->esz;
+    if (phi_kind == cudaMemcpyDeviceToDevice) {  // a device map: scan a host copy
+      staged.resize((size_t)(s->H * s->W) * s->esz);
+      if (cudaMemcpy(staged.data(), src, staged.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        s->err = "phi palette scan";
+        return fail(RD_ECUDA);
+      }
+      src = staged.data();
+    }
     for (size_t i = 0; i < vals.size(); ++i) {
       if (s->esz == 4) {
         float f;
@@ -1299,19 +1341,77 @@ const char* rd_create_error(void) { return g_create_error.c_str(); }
 const char* rd_last_error(const rd_sim* s) { return s ? s->err.c_str() : g_create_error.c_str(); }
 
 int rd_create(const rd_grid* grid, const rd_params* params, const void* phi_map, rd_sim** out) {
-  return create_common(grid, params, phi_map, 0, grid ? grid->height : 0, 0, false, out);
+  return create_common(grid, params, phi_map, 0, grid ? grid->height : 0, 0, false, out, nullptr, 0);
 }
 
 int rd_create_slab(const rd_grid* grid, const rd_params* params, const void* phi_slab, int64_t row0,
                    int64_t height_global, int32_t halo, rd_sim** out) {
-  return create_common(grid, params, phi_slab, row0, height_global, halo, true, out);
+  return create_common(grid, params, phi_slab, row0, height_global, halo, true, out, nullptr, 0);
+}
+
+int rd_arena_bytes(const rd_grid* grid, size_t* bytes) {
+  if (!grid || !bytes) return set_err(nullptr, RD_EINVAL, "grid and bytes are required");
+  if (grid->width < 3 || grid->height < 3 || grid->batch < 1 || (grid->dtype != RD_F32 && grid->dtype != RD_F64))
+    return set_err(nullptr, RD_EINVAL, "bad grid");
+  // the layout create_common computes (kept in one place: a throwaway handle
+  // description, no device work)
+  rd_sim t;
+  t.esz = grid->dtype == RD_F32 ? 4 : 8;
+  t.B = grid->batch;
+  const int64_t min_pitch = rdk::kMarginCols + grid->width + rdk::kMarginCols + 16;
+  t.pitch = grid->pitch > 0 ? grid->pitch : (min_pitch + 31) / 32 * 32;
+  const int64_t row_off = rdk::kMarginRows + rdk::kGuardRows;
+  t.plane_stride = (grid->height + 2 * row_off) * t.pitch;
+  *bytes = arena_size(&t);
+  return RD_OK;
+}
+
+int rd_create_device(const rd_grid* grid, const rd_params* params, void* arena, size_t arena_bytes,
+                     const void* phi_dev, rd_sim** out) {
+  if (!arena) return set_err(nullptr, RD_EINVAL, "arena is NULL");
+  return create_common(grid, params, phi_dev, 0, grid ? grid->height : 0, 0, false, out, arena, arena_bytes,
+                       cudaMemcpyDeviceToDevice);
+}
+
+int rd_field_ptr(rd_sim* s, int32_t b, int32_t plane, void** ptr, int64_t* pitch_elems) {
+  if (!s || !ptr) return RD_EINVAL;
+  if (int rc = check_b(s, b)) return rc;
+  void* planes[3] = {s->u[s->cur], s->v[s->cur], s->phi};
+  if (plane < 0 || plane > 2) return set_err(s, RD_EINVAL, "plane must be 0 (u), 1 (v) or 2 (phi)");
+  if (s->margins_stale && plane < 2)
+    if (int rc = fresh_margins(s)) return rc;
+  *ptr = plane_ptr(s, planes[plane], b, 0);
+  if (pitch_elems) *pitch_elems = s->pitch;
+  return RD_OK;
+}
+
+int rd_get_geometry(const rd_sim* s, rd_geometry* out) {
+  if (!s || !out) return RD_EINVAL;
+  std::memset(out, 0, sizeof *out);
+  out->width = s->W;
+  out->height = s->H;
+  out->height_global = s->Hg;
+  out->row0 = s->grow0;
+  out->batch = (int32_t)s->B;
+  out->dtype = s->g.dtype;
+  out->halo = (int32_t)s->halo;
+  out->tb_depth = s->K;
+  out->pitch = s->pitch;
+  out->rank = 0;
+  out->world = 1;
+  out->phi_rows_lo = s->slab ? std::max<int64_t>(0, s->grow0 - s->halo) - s->grow0 : 0;
+  out->phi_rows_hi = s->slab ? std::min<int64_t>(s->Hg, s->grow0 + s->H + s->halo) - s->grow0 : s->H;
+  dist_geometry(s, out);
+  return RD_OK;
 }
 
 int rd_destroy(rd_sim* s) {
   if (!s) return RD_OK;
   if (s->stream) cudaStreamSynchronize(s->stream);
+  if (s->dist) dist_destroy(s);
   for (void* m : s->ipc_mapped) cudaIpcCloseMemHandle(m);
-  void* ps[] = {s->arena,   s->tl,    s->ck_tl,  s->d_probes, s->d_first, s->d_first_ck,
+  if (s->arena && s->own_arena) cudaFree(s->arena);
+  void* ps[] = {s->tl,    s->ck_tl,  s->d_probes, s->d_first, s->d_first_ck,
                 s->d_fault, s->d_flag, s->d_scratch, s->d_idx, s->d_pal, s->d_pal_n};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -1390,6 +1490,7 @@ int rd_step(rd_sim* s, int64_t n) {
   if (!s) return RD_EINVAL;
   Range r_("rd_step");
   if (n < 0) return set_err(s, RD_EINVAL, "n must be >= 0");
+  if (s->dist) return n ? dist_step(s, n) : RD_OK;
   if (s->slab && n > s->halo) return set_err(s, RD_ERANGE, "slab handles step at most halo=%lld steps per call", (long long)s->halo);
   if (n == 0) return RD_OK;
   // slab contract: the caller refreshed the ghost rows before this call
@@ -1442,6 +1543,7 @@ int rd_step(rd_sim* s, int64_t n) {
 
 int rd_step_unchecked(rd_sim* s, int64_t n) {
   if (!s) return RD_EINVAL;
+  if (int rc = not_dist(s, "rd_step_unchecked")) return rc;
   Range r_("rd_step_unchecked");
   if (n < 0) return set_err(s, RD_EINVAL, "n must be >= 0");
   if (s->slab && n > s->halo) return set_err(s, RD_ERANGE, "slab handles step at most halo=%lld steps per call", (long long)s->halo);
@@ -1460,6 +1562,7 @@ int rd_step_unchecked(rd_sim* s, int64_t n) {
 // steps with rd_step_unchecked after the exchange.
 int rd_step_begin(rd_sim* s, int64_t k, int32_t flags, int32_t* started) {
   if (!s || !started) return RD_EINVAL;
+  if (int rc = not_dist(s, "rd_step_begin")) return rc;
   *started = 0;
   if (!s->slab) return set_err(s, RD_EINVAL, "rd_step_begin: slab handles only");
   if (s->pending_k) return set_err(s, RD_EINVAL, "rd_step_begin: a block is already open (rd_step_finish)");
@@ -1529,6 +1632,7 @@ int rd_set_peer(rd_sim* s, int32_t side, void* u0, void* u1, void* v0, void* v1,
                 int64_t plane_stride_bytes) {
   if (!s) return RD_EINVAL;
   if (side != 0 && side != 1) return set_err(s, RD_EINVAL, "side must be 0 (above) or 1 (below)");
+  if (int rc = not_dist(s, "rd_set_peer")) return rc;
   if (!s->slab) return set_err(s, RD_EINVAL, "rd_set_peer: slab handles only");
   rd_sim::Peer& p = s->peer[side];
   if (!u0) {
@@ -1581,6 +1685,7 @@ int rd_ipc_map(rd_sim* s, const void* handle64, void** mapped_base) {
 
 int rd_push_ghosts(rd_sim* s) {
   if (!s) return RD_EINVAL;
+  if (int rc = not_dist(s, "rd_push_ghosts")) return rc;
   if (!s->slab) return set_err(s, RD_EINVAL, "rd_push_ghosts: slab handles only");
   const size_t row_bytes = (size_t)s->pitch * s->esz, col = (size_t)s->col_off * s->esz;
   const size_t bytes = (size_t)s->halo * row_bytes;
@@ -1626,12 +1731,14 @@ int rd_stream_wait(rd_sim* s, void* flag, uint32_t value) {
 
 int rd_checkpoint(rd_sim* s) {
   if (!s) return RD_EINVAL;
+  if (int rc = not_dist(s, "rd_checkpoint")) return rc;
   if (int rc = sync_probes(s)) return rc;
   return save_checkpoint(s);
 }
 
 int rd_restore(rd_sim* s) {
   if (!s) return RD_EINVAL;
+  if (int rc = not_dist(s, "rd_restore")) return rc;
   return restore_checkpoint(s);
 }
 
@@ -1656,6 +1763,30 @@ int rd_get_fault(const rd_sim* s, rd_fault* out) {
 int rd_probe(rd_sim* s, int32_t b, const rd_rect* r, double threshold, int32_t* fired, double* max_u) {
   if (!s || !r) return RD_EINVAL;
   if (int rc = check_b(s, b)) return rc;
+  if (s->dist) {
+    // collective: the maximum over every rank's owned part of the rect
+    if (r->y0 >= r->y1 || r->x0 >= r->x1 || r->x0 < 0 || r->x1 > s->W || r->y0 < 0 || r->y1 > s->Hg)
+      return set_err(s, RD_ERANGE, "probe rect empty or outside the grid (SPEC.md:245-247)");
+    double m = -INFINITY;
+    rd_rect own = *r;
+    own.y0 = std::max<int64_t>(r->y0, s->grow0);
+    own.y1 = std::min<int64_t>(r->y1, s->grow0 + s->H);
+    if (own.y0 < own.y1) {
+      rd_sim* save = s;
+      DistState* d = s->dist;
+      s->dist = nullptr;  // the local probe below
+      const int rc = rd_probe(save, b, &own, threshold, nullptr, &m);
+      s->dist = d;
+      if (rc) return rc;
+      if (m != m) m = -INFINITY;  // NaN never wins (R-23)
+    }
+    std::vector<uint64_t> v{dbl_key(m)};
+    if (int rc = dist_allmax(s, v)) return rc;
+    m = key_dbl(v[0]);
+    if (max_u) *max_u = m;
+    if (fired) *fired = s->esz == 4 ? (float)m >= (float)threshold : m >= threshold;
+    return RD_OK;
+  }
   const int64_t y0 = r->y0 - s->grow0, y1 = r->y1 - s->grow0;
   if (r->y0 >= r->y1 || r->x0 >= r->x1 || r->x0 < 0 || r->x1 > s->W || y0 < 0 || y1 > s->H)
     return set_err(s, RD_ERANGE, "probe rect empty or outside the grid (SPEC.md:245-247)");
@@ -1706,6 +1837,7 @@ int rd_probe_result(rd_sim* s, int32_t id, int64_t* first) {
   long long h = -1;
   RD_CUDA(s, cudaMemcpyAsync(&h, s->d_first + id, sizeof h, cudaMemcpyDeviceToHost, s->stream));
   RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  if (s->dist) return dist_probe_result(s, h, first);  // collective: first firing over all ranks
   *first = h;
   return RD_OK;
 }
@@ -1890,3 +2022,5 @@ int rd_reset_stats(rd_sim* s) {
 }
 
 }  // extern "C"
+
+#include "rd_dist.cuh"

@@ -39,20 +39,20 @@ def test_struct_layouts_match_header():
     code = r'''
 #include <stdio.h>
 #include "rd.h"
-int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(rd_params), sizeof(rd_grid), sizeof(rd_shape),
- sizeof(rd_rect), sizeof(rd_fault), sizeof(rd_stats));return 0;}
+int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(rd_params), sizeof(rd_grid), sizeof(rd_shape),
+ sizeof(rd_rect), sizeof(rd_fault), sizeof(rd_stats), sizeof(rd_geometry));return 0;}
 '''
     exe = "/tmp/rd_sizes"
     subprocess.run(["gcc", "-x", "c", "-I", os.path.join(ROOT, "include"), "-o", exe, "-"], input=code, text=True,
                    check=True)
     sizes = list(map(int, subprocess.run([exe], capture_output=True, text=True).stdout.split()))
     ours = [C.sizeof(t) for t in (_lib.rd_params, _lib.rd_grid, _lib.rd_shape, _lib.rd_rect, _lib.rd_fault,
-                                  _lib.rd_stats)]
+                                  _lib.rd_stats, _lib.rd_geometry)]
     assert sizes == ours
 
 
 def test_abi_version_and_defaults(table1):
-    assert _lib.load().rd_abi_version() == 1
+    assert _lib.load().rd_abi_version() == 2
     p = rd.rd_params_default()
     for k in ("eps", "f", "q", "Du", "dt", "dx"):
         assert getattr(p, k) == table1[k]
@@ -83,3 +83,26 @@ def test_no_cpu_fallback(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(RuntimeError, match="not built"):
         _lib.load(str(tmp_path / "missing.so"))
+
+
+def test_dist_and_device_calls_validate_before_device():
+    """The multi-GPU and caller-memory calls reject bad arguments without a
+    device: an unknown in-process id, a rank outside the world, a NULL arena;
+    rd_arena_bytes needs no device at all; the in-process id is tagged."""
+    uid = rd.rd_dist_local_id()
+    assert uid[:8] == b"RDLOCAL1" and len(uid) == 128
+    bogus = b"RDLOCAL1" + b"\xff" * 8 + bytes(112)
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create_dist(64, 64, None, 0, 2, bogus)
+    assert e.value.code == _lib.RD_EINVAL
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create_dist(64, 64, None, 3, 2, uid)
+    assert e.value.code == _lib.RD_EINVAL
+    with pytest.raises(ValueError):
+        rd.rd_create_dist(64, 64, np.zeros((10, 64), np.float32), 0, 2, uid)  # not the 32 owned rows
+    n = rd.rd_arena_bytes(100, 50, dtype=np.float32)
+    pitch = (8 + 100 + 8 + 16 + 31) // 32 * 32
+    assert n == 7 * (50 + 2 * (8 + 24)) * pitch * 4 + 256
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create_device(100, 50, 0, n, None)
+    assert e.value.code == _lib.RD_EINVAL

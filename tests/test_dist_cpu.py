@@ -18,7 +18,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_1901_06535_b200.dist import exchange, exchange_plan, ghost_extent, slab_rows
+from paper_1901_06535_b200.dist import exchange_plan, ghost_extent, slab_rows
+from slab_protocol import exchange
 from rdinputs import half_discs, noise_plane
 
 H, W, STEPS = 37, 53, 23

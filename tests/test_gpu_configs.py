@@ -99,7 +99,7 @@ def test_config5_full_size_sampled_blocks(path):
     import torch
     import paper_1901_06535_b200 as rd
     import oracle
-    from paper_1901_06535_b200.dist import SlabSim, _dev_rows
+    from slab_protocol import SlabSim, _dev_rows
     n, S = 24, 16
     w = config(5, steps=n)
     H, W = w.H, w.W

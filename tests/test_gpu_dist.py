@@ -8,7 +8,7 @@ import pytest
 import oracle
 import paper_1901_06535_b200 as rd
 from gpu_util import assert_bitwise
-from paper_1901_06535_b200.dist import LoopbackGroup, SlabSim
+from slab_protocol import LoopbackGroup, SlabSim
 from rdinputs import half_discs, noise_plane, obstacles
 
 pytestmark = pytest.mark.gpu

@@ -39,7 +39,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
-        from paper_1901_06535_b200.dist import SlabSim
+        from slab_protocol import SlabSim
         sl = SlabSim(W, H, rank, world, _phi, dtype=np.float32, halo=4)
         sl.fill_noise(seed=2)
         for s, val, at in _events():
@@ -126,7 +126,7 @@ def _ipc_worker(rank, world, port, q):
     try:
         torch.cuda.set_device(0)
         import paper_1901_06535_b200 as rd
-        from paper_1901_06535_b200.dist import SlabSim
+        from slab_protocol import SlabSim
         H2, W2, halo = 64, 100, 4
         sl = SlabSim(W2, H2, rank, world, lambda b, r0, n: np.full((n, W2), 0.054), dtype=np.float32, halo=halo,
                      p2p=True)  # maps the neighbour's plane allocation (CUDA IPC)
@@ -138,7 +138,7 @@ def _ipc_worker(rank, world, port, q):
             rd.rd_stream_signal(sl.h, f, 41 + rank)  # into the neighbour's flag word
         torch.cuda.synchronize()
         dist.barrier()  # the hosts order the two processes: no GPU work waits on the other
-        from paper_1901_06535_b200.dist import _DevRows, _dev_rows
+        from slab_protocol import _DevRows, _dev_rows
         r0 = -halo if rank == 1 else sl.rows
         ghost = _dev_rows(sl.h, 0, 0, r0, r0 + halo).cpu().numpy()  # row storage, ghost columns included
         rows = ghost.view(np.float32).reshape(halo, -1)

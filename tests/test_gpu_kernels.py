@@ -218,6 +218,22 @@ def test_c_abi_from_plain_c(tmp_path):
     assert "C ABI ok" in out.stdout
 
 
+def test_c_dist_abi_from_plain_c(tmp_path):
+    """The multi-GPU calls from C (tests/c/dist_c_demo.c): rd_dist_unique_id +
+    rd_create_dist at world 1 over NCCL, and two in-process ranks
+    (rd_dist_local_id, pthreads) on one device in fp32 and fp64 -- each
+    bitwise equal to the oracle's C library on the whole grid."""
+    root = os.path.dirname(HERE)
+    exe = str(tmp_path / "dist_c_demo")
+    lib, orc = os.path.join(root, "paper_1901_06535_b200"), os.path.join(root, "oracle")
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(root, "include"), "-I", orc,
+                    os.path.join(HERE, "c", "dist_c_demo.c"), "-L", lib, "-lrd", "-L", orc, "-lorc", "-lpthread",
+                    f"-Wl,-rpath,{lib}:{orc}", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "C dist ABI ok" in out.stdout
+
+
 @pytest.fixture(scope="module")
 def divcheck64(tmp_path_factory):
     exe = str(tmp_path_factory.mktemp("cuda64") / "divcheck64")
