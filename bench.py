@@ -8,9 +8,13 @@ One bench "step" = rd_step(T) with T = --timesteps (default 1000) time steps of
 the whole hot path (a1-a8: due stimuli, K-step blocked stencil launches, the
 non-finite health check, probe latches) over the workload:
   N = 1: configs[3] "c4_roofline" 16384 x 16384 fp32, noise + 64 half-discs;
-         K = 10 x 1000 = the config's 10000 timed steps.
-  N > 1: configs[4] weak scaling: a 16384-row slab per GPU of a
-         (16384 N) x 16384 grid with 16 N obstacles, halo exchange over NCCL.
+         K = 10 x 1000 = the config's 10000 timed steps. The line also carries
+         per_config (configs[0..2] in fp32 and fp64: rate, kernel, probe
+         outcomes vs the paper's, the oracle's rate) and fp32_error (R-17).
+  N > 1: configs[4] weak scaling, a 16384-row slab per GPU of a
+         (16384 N) x 16384 grid with 16 N obstacles, each rank an
+         rd_create_dist handle (halo exchange inside librd); beside it
+         "strong": configs[4] at 65536 x 65536 split over the N GPUs.
 Inputs (5 planes x 1 GiB per GPU) are far larger than L2 (126 MB), so no
 flush is needed between steps. Rank 0 prints ONE JSON line.
 """
@@ -114,23 +118,24 @@ def dist_env():
     return world, rank, local
 
 
-def config_dict(world: int, T: int, tb_depth: int, scaling: str = "weak") -> dict:
+def config_dict(world: int, T: int, tb_depth: int, scaling: str = "weak", strong_grid: int = 65536) -> dict:
     """The `config` of the JSON line -- the same for our arm and the
     reference arm (BASELINE.json configs[3] at N = 1,
     configs[4] weak scaling at N > 1; --scaling strong: configs[4] at its full
     65536 x 65536 over N GPUs)."""
     if scaling == "strong":
-        d = {"workload": "configs[4] strong scaling: 65536x65536 fp32 row slabs over N GPUs, 256 obstacles "
-                         "phi=0.2, masked half-discs, NCCL halo exchange", "grid": [65536, 65536]}
+        G = strong_grid
+        d = {"workload": f"configs[4] strong scaling: {G}x{G} fp32 row slabs over N GPUs (rd_create_dist), "
+                         "256 obstacles phi=0.2 per 65536^2, masked half-discs", "grid": [G, G]}
         return dict(d, time_steps_per_step=T, tb_depth=tb_depth,
-                    l2="inputs larger than L2 (5 planes of 17/N GB per GPU); no flush needed",
+                    l2=f"inputs larger than L2 (5 planes of {G * G * 4 / 1e9:.1f}/N GB per GPU); no flush needed",
                     parallelism=f"row slabs x{world}")
     if world == 1:
         d = {"workload": "configs[3] c4_roofline: 16384x16384 fp32, phi=0.054, u,v~U[0,0.1) seed 1, "
                          "64 half-discs r=8 seed 2, no-flux", "grid": [16384, 16384]}
     else:
-        d = {"workload": f"configs[4] weak scaling: ({16384 * world})x16384 fp32 row slabs, 16 obstacles/GPU "
-                         "phi=0.2, masked half-discs, NCCL halo exchange", "grid": [16384 * world, 16384]}
+        d = {"workload": f"configs[4] weak scaling: ({16384 * world})x16384 fp32 row slabs (rd_create_dist), "
+                         "16 obstacles/GPU phi=0.2, masked half-discs", "grid": [16384 * world, 16384]}
     return dict(d, time_steps_per_step=T, tb_depth=tb_depth,
                 l2="inputs larger than L2 (5 x 1 GiB planes per GPU); no flush needed",
                 parallelism=f"row slabs x{world}" if world > 1 else "single GPU")
@@ -154,6 +159,65 @@ def max_over_ranks(x: float, world: int) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+# ------------------------------------------------------------- rank context
+
+class ProcCtx:
+    """One process per GPU (the driver's torchrun launch): torch.distributed
+    for the rendezvous id, barriers and the max over ranks -- never for the
+    halo data, which librd moves itself (rd_create_dist)."""
+
+    def __init__(self, world, rank, local):
+        self.world, self.rank, self.local, self.functional = world, rank, local, False
+
+    def barrier(self):
+        import torch
+        torch.cuda.synchronize()
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max(self, x: float) -> float:
+        return max_over_ranks(x, self.world)
+
+    def uid(self) -> bytes:
+        from paper_1901_06535_b200.dist import unique_id
+        return unique_id()
+
+
+class ThreadCtx:
+    """RD_BENCH_THREADS=1: the N ranks as host threads of ONE process on one
+    GPU (rd_dist_local_id) -- a functional check of the N > 1 code path and
+    its JSON line on a one-GPU box, not a measurement (the ranks share SMs)."""
+
+    def __init__(self, world, rank, shared):
+        self.world, self.rank, self.local, self.functional = world, rank, 0, True
+        self.shared = shared
+
+    def barrier(self):
+        import torch
+        torch.cuda.synchronize()
+        self.shared["barrier"].wait()
+        torch.cuda.synchronize()
+
+    def max(self, x: float) -> float:
+        sh = self.shared
+        sh["vals"][self.rank] = x
+        sh["barrier"].wait()
+        m = max(sh["vals"])
+        sh["barrier"].wait()
+        return m
+
+    def uid(self) -> bytes:
+        import paper_1901_06535_b200 as rd
+        if self.rank == 0:
+            self.shared["uid"] = rd.rd_dist_local_id()
+        self.shared["barrier"].wait()
+        u = self.shared["uid"]
+        self.shared["barrier"].wait()
+        return u
 
 
 # ------------------------------------------------------------- our arm
@@ -226,178 +290,394 @@ def e2e_pipelined(rd, sim, w, dtype, tb, pu, pv, T, depth, steps, cells):
                    "rd_read_fields(host) every step"}
 
 
-def run_ours(args):
-    import torch
-    import paper_1901_06535_b200 as rd
-    from paper_1901_06535_b200.dist import SlabSim
-    from rdinputs import config
+def load_traffic(workload: str, kernel: str, cells_per_launch: float):
+    """DRAM bytes per launch of `kernel` on `workload` from a committed ncu
+    --set full capture (profiles/traffic_rNN.json) -- only if the capture is
+    of this very workload, kernel and launch size (its cell-update count
+    stored beside it); else None."""
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")), reverse=True):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        for e in d.get("entries", []):
+            if (e.get("workload") == workload and e.get("kernel") == kernel
+                    and abs(e.get("cell_updates_per_launch", -1) - cells_per_launch) < 0.5):
+                return e["dram_bytes_per_launch"], os.path.relpath(f, ROOT)
+    return None, None
 
-    world, rank, local = dist_env()
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        # RD_BENCH_BACKEND=gloo: functional check of this N > 1 path with
-        # several ranks on one GPU (host-staged halos; not a measurement)
-        backend = os.environ.get("RD_BENCH_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    dtype = np.dtype(np.float32)
-    T = args.timesteps
+
+def roofline_of(st, ms, workload_tag, dtype):
+    """ALU roofline of the dominant kernel with the one-step
+    HBM view beside it, from the stencil launches' summed CUDA-event times
+    inside the timed region (rd_set_profiling)."""
     hbm, hbm_src = peaks()
-
-    strong = args.scaling == "strong"
-    if world == 1 and not strong:
-        w = config(4)
-        H, W = w.H, w.W
-        # inputs built on the device: phi = 0.054, seeded U[0,0.1) noise
-        # (rd_fill_noise == rdinputs.noise_plane bitwise), 64 half-discs
-        sim = rd.Sim(None, shape=(1, H, W), dtype=dtype, tb_depth=args.tb)
-        h = sim.h
-        sim.paint_phi(0.054)
-        sim.fill_noise(seed=1)
-        u0, v0 = sim.read(0)  # host copies for the e2e leg and the CPU baseline
-        phi = np.full((H, W), 0.054, dtype=dtype)
-        for shape, val, at in w.events[0]:
-            sim.stimulate(shape, val, at)
-        stepper = sim.step
-        cells = H * W
-    else:
-        # weak: 16384 rows per GPU; strong: the full 65536^2 grid split over
-        # the ranks (N = 1 included: one 120 GB slab)
-        w = (config(5) if strong else config(5, H=16384 * world, W=16384, n_obstacles=16 * world))
-        H, W = w.H, w.W
-        slab = SlabSim(W, H, rank, world, None, dtype=dtype, halo=max(args.tb, 4) if args.tb else 4,
-                       p2p=args.p2p)
-        h = slab.h
-        rd.rd_paint_phi(h, -1, None, 0.054)
-        for rect in w.meta["obstacles"]:
-            rd.rd_paint_phi(h, -1, rect, 0.2)
-        slab.fill_noise(seed=1)
-        for shape, val, at in w.events[0]:
-            slab.stimulate(shape, val, at)
-        stepper = slab.step
-        cells = slab.rows * W
-        # host copies of this rank's rows for the e2e leg (not at the strong
-        # sizes: 17/N GB per plane)
-        u0 = v0 = None
-        if not strong:
-            u0, v0 = slab.read_owned(0)
-    stream = torch.cuda.current_stream()
-    rd.rd_set_stream(h, rd.stream_handle(stream))  # engine work on the stream the events are recorded on
-
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-            torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        stepper(T)
-    barrier()
-    rd.rd_reset_stats(h)
-    rd.rd_set_profiling(h, True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            stepper(T)
-        e1.record(stream)
-        barrier()
-    ms = e0.elapsed_time(e1)
-    st = rd.rd_get_stats(h)
-    rd.rd_set_profiling(h, False)
-    ms_max = max_over_ranks(ms, world)
-    total_updates = cells * world * T * args.steps
-    value = total_updates / (ms_max / 1e3) / 1e9
-
-    # dominant kernel: the temporally blocked stencil (tb_kernel)
     kms = st["step_kernel_ms"]
     k_launches = max(1, st["timed_launches"])
     bpc = BYTES_PER_CELL[dtype]
     achieved = bpc * st["cell_updates"] / (kms / 1e3) / 1e9 if kms > 0 else None
-    # DRAM bytes per tb_kernel launch from the latest committed ncu --set full
-    # capture (profiles/traffic_rNN.json, scripts/summarize_ncu.py)
-    traffic = None
-    tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))
-    if tfiles:
-        try:
-            traffic = json.load(open(tfiles[-1])).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    # temporal blocking moves the kernel off the HBM roof (DRAM bytes per
-    # launch ~ one step's, ncu) onto the FP32 pipe: report the ALU bound, with
-    # the one-step HBM view beside it
     alu, alu_src = alu_peak_tops()
     ops = OPS_PER_CELL * st["cell_updates"] / (kms / 1e3) / 1e12 if kms > 0 else None
-    roofline = {"bound": "alu", "achieved": ops, "peak": alu, "unit": "TFLOP/s",
-                "frac": (ops / alu) if ops else None, "traffic": traffic,
-                "kernel": f"tb_kernel<float,K={st['tb_depth']}>", "peak_source": alu_src,
-                "algorithmic_ops_per_cell_update": OPS_PER_CELL,
-                "ops": "fp32 add/sub/mul/div of the canonical Eq.-1 tree (13 + 9 + 1), R-8",
-                "cell_updates_per_launch": st["cell_updates"] / k_launches,
-                "avg_launch_ms": kms / k_launches, "kernel_share_of_step": kms / ms if ms else None,
-                "hbm_view": {"achieved": achieved, "peak": hbm, "unit": "GB/s",
-                             "frac": (achieved / hbm) if achieved else None, "peak_source": hbm_src,
-                             "algorithmic_bytes_per_cell_update": bpc, "one_step_roofline_gcells": hbm / bpc}}
+    kernel = f"tb_kernel<float,K={st['tb_depth']}>"
+    cpl = st["cell_updates"] / k_launches
+    traffic, tsrc = load_traffic(workload_tag, kernel, cpl)
+    return {"bound": "alu", "achieved": ops, "peak": alu, "unit": "TFLOP/s",
+            "frac": (ops / alu) if ops else None, "traffic": traffic,
+            "traffic_source": tsrc or "no ncu capture of this workload/kernel/launch size: null",
+            "kernel": kernel, "peak_source": alu_src,
+            "algorithmic_ops_per_cell_update": OPS_PER_CELL,
+            "ops": "fp32 add/sub/mul/div of the canonical Eq.-1 tree (13 + 9 + 1), R-8",
+            "cell_updates_per_launch": cpl, "avg_launch_ms": kms / k_launches,
+            "kernel_share_of_step": kms / ms if ms else None,
+            "hbm_view": {"achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": (achieved / hbm) if achieved else None, "peak_source": hbm_src,
+                         "algorithmic_bytes_per_cell_update": bpc, "one_step_roofline_gcells": hbm / bpc}}
+
+
+def timed(ctx, stepper, h, T, steps, warmup, clocks_index):
+    """W warm-up steps, then K steps bracketed by barrier + synchronize, CUDA
+    events on the engine's stream (torch's current), clocks sampled during
+    the timed region. Returns (device ms of this rank, stats, clocks)."""
+    import torch
+    import paper_1901_06535_b200 as rd
+    stream = torch.cuda.current_stream()
+    rd.rd_set_stream(h, rd.stream_handle(stream))
+    for _ in range(warmup):
+        stepper(T)
+    ctx.barrier()
+    rd.rd_reset_stats(h)
+    rd.rd_set_profiling(h, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = Clocks(clocks_index) if ctx.rank == 0 else None
+    if clk:
+        clk.__enter__()
+    try:
+        ctx.barrier()
+        e0.record(stream)
+        for _ in range(steps):
+            stepper(T)
+        e1.record(stream)
+        ctx.barrier()
+    finally:
+        if clk:
+            clk.__exit__()
+    ms = e0.elapsed_time(e1)
+    st = rd.rd_get_stats(h)
+    rd.rd_set_profiling(h, False)
+    return ms, st, (clk.summary() if clk else None)
+
+
+def per_config(cpu_seconds: float):
+    """configs[0..2] -- the 128^2 disc, the AND-gate batch and the diode batch
+    (§4) -- in fp32 and fp64 through rd_step, each run in
+    full (second of two runs: the first warms module loads and clocks): device
+    time, Gcell/s, the stencil kernel, the probe outcomes against the paper's
+    (rdinputs expect), and the oracle's own rate on the host cores on a
+    bounded sample of the same instance (cpu_baseline)."""
+    import torch
+    import paper_1901_06535_b200 as rd
+    from rdinputs import config
+    out = []
+    for n in (1, 2, 3):
+        for dt in (np.float32, np.float64):
+            w = config(n, dtype=dt)
+            phi = np.stack([w.phi_plane(b).astype(dt) for b in range(w.B)])
+            for rep in range(2):
+                sim = rd.Sim(phi, dtype=dt)
+                for b in range(w.B):
+                    for shape, val, at in w.events[b]:
+                        sim.stimulate(shape, val, at, b=b)
+                pids = ([[sim.probe_latch(b, r, t, s) for (r, t, s) in w.probes[b]] for b in range(w.B)]
+                        if w.probes else [])
+                stream = torch.cuda.current_stream()
+                sim.set_stream(stream)
+                rd.rd_reset_stats(sim.h)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                sim.step(w.steps)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1)
+                st = sim.stats()
+                fires = [[sim.probe_result(p) for p in ps] for ps in pids]
+                sim.close()
+            cells = w.B * w.H * w.W * w.steps
+            got = [any(f >= 0 for f in fs) for fs in fires] if fires else None
+            exp = w.expect.get("fires")
+            e = {"config": f"configs[{n - 1}] {w.name}", "dtype": np.dtype(dt).name, "batch": w.B,
+                 "grid": [w.H, w.W], "time_steps": w.steps, "device_ms": ms,
+                 "gcell_updates_per_s": cells / (ms / 1e3) / 1e9,
+                 "stencil_kernel": ["tb_kernel", "lp_kernel", "cr_kernel"][st["kernel"]],
+                 "kernel_launches": st["launches"], "first_fire": fires, "fires": got, "expected_fires": exp,
+                 "outcome_ok": (got == exp) if exp is not None else None}
+            if cpu_seconds > 0:
+                e["cpu_baseline"] = oracle_rate(w, dt, cpu_seconds)
+            out.append(e)
+    return out
+
+
+def oracle_rate(w, dt, seconds: float):
+    """The oracle (as it stands, on all host cores) on instance 0 of w for a
+    bounded number of its steps."""
+    import oracle
+    oracle.set_num_threads(host_cores())
+    u0, v0 = w.init_planes(0)
+    phi = w.phi_plane(0).astype(dt)
+    t = time.perf_counter()
+    oracle.run(u0.astype(dt), v0.astype(dt), phi, 20, events=w.events[0])
+    t1 = (time.perf_counter() - t) / 20
+    n = int(max(20, min(w.steps, seconds / max(t1, 1e-6))))
+    t = time.perf_counter()
+    oracle.run(u0.astype(dt), v0.astype(dt), phi, n, events=w.events[0])
+    el = time.perf_counter() - t
+    return {"value": w.H * w.W * n / el / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"instance 0, first {n} of {w.steps} time steps"}
+
+
+def fp32_error():
+    """BASELINE.json north_star's literal fp32 check, reported (reading R-17):
+    max |u_fp32 - u_fp64| on config 1 after 300 and 1000 steps, both computed
+    by this engine (its fp64 path equals the fp64 oracle bitwise; its fp32
+    path the oracle's fp32 mode)."""
+    import paper_1901_06535_b200 as rd
+    from rdinputs import config
+    res = {}
+    for steps in (300, 1000):
+        f = {}
+        for dt in (np.float32, np.float64):
+            w = config(1, dtype=dt)
+            with rd.Sim(w.phi_plane(0).astype(dt)[None], dtype=dt) as sim:
+                for shape, val, at in w.events[0]:
+                    sim.stimulate(shape, val, at)
+                sim.step(steps)
+                f[dt] = sim.read(0)
+        du = np.abs(f[np.float32][0].astype(np.float64) - f[np.float64][0])
+        dv = np.abs(f[np.float32][1].astype(np.float64) - f[np.float64][1])
+        res[f"step{steps}"] = {"max_abs_du": float(du.max()), "max_abs_dv": float(dv.max()),
+                               "cells_over_2e-3": int(np.count_nonzero(np.maximum(du, dv) > 2e-3))}
+    res.update(tolerance=2e-3, config="configs[0] 128x128 disc",
+               reading="DESIGN.md R-17: gated bitwise against the oracle's fp32 mode and <= 2e-3 vs fp64 up to "
+                       "step 300; the step-1000 gap is the refractory wake amplifying rounding, reported not gated")
+    return res
+
+
+def run_single(args):
+    """N = 1: configs[3] (16384^2 fp32) -- the metric's own configuration."""
+    import torch
+    import paper_1901_06535_b200 as rd
+    from rdinputs import config
+    ctx = ProcCtx(1, 0, 0)
+    dtype = np.dtype(np.float32)
+    T = args.timesteps
+    w = config(4)
+    H, W = w.H, w.W
+    # inputs built on the device: phi = 0.054, seeded U[0,0.1) noise
+    # (rd_fill_noise == rdinputs.noise_plane bitwise), 64 half-discs
+    sim = rd.Sim(None, shape=(1, H, W), dtype=dtype, tb_depth=args.tb)
+    h = sim.h
+    sim.paint_phi(0.054)
+    sim.fill_noise(seed=1)
+    u0, v0 = sim.read(0)  # host copies for the e2e leg and the CPU baseline
+    phi = np.full((H, W), 0.054, dtype=dtype)
+    for shape, val, at in w.events[0]:
+        sim.stimulate(shape, val, at)
+    cells = H * W
+    ms, st, clk = timed(ctx, sim.step, h, T, args.steps, args.warmup, 0)
+    value = cells * T * args.steps / (ms / 1e3) / 1e9
+    roofline = roofline_of(st, ms, "c4_roofline", dtype)
+    stream = torch.cuda.current_stream()
 
     # e2e through the public API with pinned host buffers: every step writes
-    # this rank's u, v from the host, steps, and reads u, v back (N > 1: the
-    # owned rows of each slab; time = max over ranks)
+    # u, v from the host, steps, and reads u, v back
     e2e = None
-    if strong:
-        e2e = {"skipped": "--scaling strong: 65536^2 host copies (17/N GB per plane) are not staged; "
-                          "the default (weak) line carries e2e"}
-    elif args.e2e_steps > 0:
-        rows = u0.shape[0]
-        pu = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
-        pv = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
+    if args.e2e_steps > 0:
+        pu = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+        pv = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
         pu[...] = u0
         pv[...] = v0
-        ou = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
-        ov = torch.empty((rows, W), dtype=torch.float32, pin_memory=True).numpy()
-        barrier()
+        ou = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+        ov = torch.empty((H, W), dtype=torch.float32, pin_memory=True).numpy()
+        ctx.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.e2e_steps):
             rd.rd_write_fields(h, 0, pu, pv)
-            stepper(T)
+            sim.step(T)
             rd.rd_read_fields(h, 0, ou, ov)
         b.record(stream)
-        barrier()
-        ems = max_over_ranks(a.elapsed_time(b), world)
-        e2e = {"value": cells * world * T * args.e2e_steps / (ems / 1e3) / 1e9, "unit": UNIT,
+        ctx.barrier()
+        ems = a.elapsed_time(b)
+        e2e = {"value": cells * T * args.e2e_steps / (ems / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 2 * cells * 4, "d2h_bytes_per_step": 2 * cells * 4,
-               "steps": args.e2e_steps,
-               "api": ("rd_write_fields(host pinned) + rd_step + rd_read_fields(host)" if world == 1 else
-                       "per rank: rd_write_fields(host pinned, owned rows) + SlabSim.step (NCCL halos) + "
-                       "rd_read_fields(host); bytes per rank, time max over ranks")}
-        if world == 1 and args.e2e_pipeline > 1:
+               "steps": args.e2e_steps, "api": "rd_write_fields(host pinned) + rd_step + rd_read_fields(host)"}
+        if args.e2e_pipeline > 1:
             serial = e2e
-            e2e = e2e_pipelined(rd, sim, w, dtype, args.tb, pu, pv, T, args.e2e_pipeline, args.e2e_pipeline_steps, cells)
+            e2e = e2e_pipelined(rd, sim, w, dtype, args.tb, pu, pv, T, args.e2e_pipeline, args.e2e_pipeline_steps,
+                                cells)
             e2e["serial"] = {"value": serial["value"], "steps": serial["steps"], "api": serial["api"]}
-
-    cpu = None
-    if rank == 0 and world == 1 and not strong and not args.no_cpu_baseline:
-        cpu = cpu_baseline(u0, v0, phi, args.cpu_seconds)
-
     launches = st["launches"]
-    if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_dict(world, T, st["tb_depth"], args.scaling),
-                "frac_of_one_step_hbm_roofline": value / world / (hbm / bpc),
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary()}
+    sim.close()
+    cpu = None if args.no_cpu_baseline else cpu_baseline(u0, v0, phi, args.cpu_seconds)
+    hbm, _ = peaks()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(1, T, st["tb_depth"]),
+            "frac_of_one_step_hbm_roofline": value / (hbm / BYTES_PER_CELL[dtype]),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+    if not args.no_configs:
+        line["per_config"] = per_config(0 if args.no_cpu_baseline else args.config_cpu_seconds)
+        line["fp32_error"] = fp32_error()
+    return line
+
+
+def dist_run(args, ctx, strong: bool):
+    """One N > 1 line: configs[4] weak (16384 rows per GPU) or strong (the
+    --strong-grid^2 grid, 65536^2 by default, split over the ranks), each rank
+    an rd_create_dist slab; rd_step runs the whole distributed super-step in
+    librd. Returns this rank's timing and stats."""
+    import torch
+    import paper_1901_06535_b200 as rd
+    from paper_1901_06535_b200.dist import DistSim
+    from rdinputs import config
+    world, rank = ctx.world, ctx.rank
+    dtype = np.dtype(np.float32)
+    T = args.strong_timesteps if strong else args.timesteps
+    if strong:
+        G = args.strong_grid
+        w = config(5, H=G, W=G, n_obstacles=max(1, 256 * G * G // (65536 * 65536)))
+    else:
+        w = config(5, H=16384 * world, W=16384, n_obstacles=16 * world)
+    H, W = w.H, w.W
+    sim = DistSim(W, H, rank, world, None, uid=ctx.uid(), dtype=dtype, tb_depth=args.tb)
+    try:
+        sim.paint_phi(0.054)
+        for rect in w.meta["obstacles"]:
+            sim.paint_phi(0.2, rect)
+        sim.fill_noise(seed=1)
+        for shape, val, at in w.events[0]:
+            sim.stimulate(shape, val, at)
+        cells = sim.rows * W
+        u0 = v0 = None
+        if not strong and args.e2e_steps > 0:
+            u0, v0 = sim.read_owned(0)
+        ms, st, clk = timed(ctx, sim.step, sim.h, T, args.steps, args.warmup, ctx.local)
+        ms_max = ctx.max(ms)
+        geo = sim.geometry()
+        e2e = None
+        if not strong and args.e2e_steps > 0:
+            # per rank: owned rows in from pinned host memory, step (halos
+            # inside librd), owned rows out; max over ranks
+            pu = torch.empty((sim.rows, W), dtype=torch.float32, pin_memory=True).numpy()
+            pv = torch.empty((sim.rows, W), dtype=torch.float32, pin_memory=True).numpy()
+            pu[...] = u0
+            pv[...] = v0
+            ou = np.empty_like(pu)
+            ov = np.empty_like(pv)
+            stream = torch.cuda.current_stream()
+            ctx.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.e2e_steps):
+                rd.rd_write_fields(sim.h, 0, pu, pv)
+                sim.step(T)
+                rd.rd_read_fields(sim.h, 0, ou, ov)
+            b.record(stream)
+            ctx.barrier()
+            ems = ctx.max(a.elapsed_time(b))
+            e2e = {"value": H * W * T * args.e2e_steps / (ems / 1e3) / 1e9, "unit": UNIT,
+                   "h2d_bytes_per_step": 2 * cells * 4, "d2h_bytes_per_step": 2 * cells * 4,
+                   "steps": args.e2e_steps,
+                   "api": "per rank: rd_write_fields(host pinned, owned rows) + rd_step (rd_create_dist: halos "
+                          "inside librd) + rd_read_fields(host); bytes per rank, time max over ranks"}
+    finally:
+        sim.close()
+    value = H * W * T * args.steps / (ms_max / 1e3) / 1e9
+    return {"value": value, "ms_per_step": ms_max / args.steps, "rank_ms_per_step": ms / args.steps,
+            "T": T, "grid": [H, W], "st": st, "clk": clk, "geo": geo, "e2e": e2e,
+            "roofline": roofline_of(st, ms, "c5_strong" if strong else "c5_weak", dtype)}
+
+
+def run_dist(args, ctx):
+    """N > 1 (and --scaling strong at N = 1): the weak line with the strong
+    result beside it (BASELINE.json north_star: "8-GPU scaling efficiency
+    >=85% on the largest grid" is the strong number)."""
+    world = ctx.world
+    hbm, _ = peaks()
+    weak = None if args.scaling == "strong" else dist_run(args, ctx, strong=False)
+    strong = None
+    if args.scaling == "strong" or (world > 1 and not args.no_strong):
+        strong = dist_run(args, ctx, strong=True)
+    if ctx.rank != 0:
+        return None
+    main = weak or strong
+    scaling = "weak" if weak else "strong"
+    st = main["st"]
+    line = {"metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(world, main["T"], st["tb_depth"], scaling, args.strong_grid),
+            "frac_of_one_step_hbm_roofline": main["value"] / world / (hbm / BYTES_PER_CELL[np.dtype(np.float32)]),
+            "roofline": main["roofline"], "cpu_baseline": None, "e2e": main["e2e"],
+            "gpu_launches": st["launches"], "clocks": main["clk"],
+            "transport": main["geo"]["transport"], "halo_exchanges_rank0": main["geo"]["exchanges"]}
+    if main["e2e"] is None:
+        line["e2e"] = {"skipped": "--scaling strong: host copies of the 65536^2 grid (17/N GB per plane) are "
+                                  "not staged; the weak line carries e2e"}
+    if weak and strong:
+        line["strong"] = {"value": strong["value"], "unit": UNIT, "ms_per_step": strong["ms_per_step"],
+                          "rank0_ms_per_step": strong["rank_ms_per_step"], "time_steps_per_step": strong["T"],
+                          "config": config_dict(world, strong["T"], strong["st"]["tb_depth"], "strong",
+                                                args.strong_grid),
+                          "roofline": strong["roofline"], "transport": strong["geo"]["transport"]}
+    if ctx.functional:
+        line["functional_check"] = ("RD_BENCH_THREADS: the ranks ran as threads on ONE GPU; the numbers are not "
+                                    "a measurement")
+    return line
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    threads = os.environ.get("RD_BENCH_THREADS") == "1" and args.gpus > 1
+    if threads:
+        world = args.gpus
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world == 1 and args.scaling != "strong":
+        line = run_single(args)
+    elif threads:
+        shared = {"barrier": threading.Barrier(world), "vals": [0.0] * world}
+        out = [None] * world
+        errs = []
+
+        def body(r):
+            try:
+                torch.cuda.set_device(local)
+                out[r] = run_dist(args, ThreadCtx(world, r, shared))
+            except BaseException as e:  # noqa: BLE001 -- surfaced below
+                errs.append(e)
+                shared["barrier"].abort()
+
+        ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            raise errs[0]
+        line = out[0]
+    else:
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        line = run_dist(args, ProcCtx(world, rank, local))
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if line is not None:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
 
 
 def cpu_baseline(u0, v0, phi, seconds: float):
@@ -482,10 +762,15 @@ def main():
     ap.add_argument("--e2e-pipeline-steps", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--p2p", action="store_true",
-                    help="N > 1: peer-memory halo push (CUDA IPC + stream-ordered flags) instead of NCCL")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N > 1 workload: configs[4] weak (16384 rows per GPU, default) or strong (65536^2 split)")
+                    help="the line's workload: weak (N = 1: configs[3]; N > 1: configs[4] with 16384 rows per GPU, "
+                         "the strong result beside it) or strong (configs[4] 65536^2 split over N, any N)")
+    ap.add_argument("--strong-grid", type=int, default=65536, help="side of the strong-scaling grid")
+    ap.add_argument("--strong-timesteps", type=int, default=200, help="time steps per bench step, strong line")
+    ap.add_argument("--no-strong", action="store_true", help="N > 1: skip the strong-scaling result")
+    ap.add_argument("--no-configs", action="store_true", help="N = 1: skip per_config and fp32_error")
+    ap.add_argument("--config-cpu-seconds", type=float, default=2.0,
+                    help="oracle seconds per per_config entry (its cpu_baseline)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

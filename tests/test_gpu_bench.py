@@ -24,7 +24,7 @@ def _line(args, timeout=600):
 
 def test_bench_line_has_the_contract_keys():
     d = _line(["--timesteps", "20", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "1",
-               "--e2e-pipeline-steps", "3"])
+               "--e2e-pipeline-steps", "3", "--config-cpu-seconds", "0.2"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
@@ -35,6 +35,8 @@ def test_bench_line_has_the_contract_keys():
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in r, k
     assert r["bound"] in ("alu", "hbm", "tensor") and 0 < r["frac"] and r["achieved"] > 0 and r["peak"] > 0
+    # traffic is the committed ncu capture of this very workload/kernel/launch size, or null
+    assert r["traffic"] is None or r["traffic"] > 16384 * 16384 * 16
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] >= 1 and c["sample"]
     e = d["e2e"]
@@ -42,6 +44,36 @@ def test_bench_line_has_the_contract_keys():
     assert e["pipeline"] == 2 and e["steps"] == 3 and e["serial"]["value"] > 0 and e["serial"]["steps"] == 1
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    # configs[0..2] in both precisions, with the paper's outcomes
+    pc = d["per_config"]
+    assert len(pc) == 6 and {x["dtype"] for x in pc} == {"float32", "float64"}
+    for x in pc:
+        assert x["gcell_updates_per_s"] > 0 and x["cpu_baseline"]["value"] > 0
+        if x["expected_fires"] is not None:
+            assert x["outcome_ok"] is True, x
+    f = d["fp32_error"]
+    assert f["step300"]["max_abs_du"] <= 2e-3 and f["step1000"]["max_abs_du"] > 0
+
+
+def test_bench_n2_line_as_threads_on_one_gpu():
+    """The N > 1 code path (weak line + strong result, rd_create_dist ranks)
+    with its two ranks as threads of one process on this box's one GPU
+    (RD_BENCH_THREADS): a functional check of the line, not a measurement.
+    The driver's real N > 1 launch is torchrun with one process per GPU."""
+    env = dict(os.environ, RD_BENCH_THREADS="1")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--timesteps", "8",
+                          "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--strong-grid", "8192",
+                          "--strong-timesteps", "8"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["steps"] == 3
+    assert "configs[4]" in d["config"]["workload"] and d["functional_check"]
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0 and d["transport"] == "local"
+    assert d["halo_exchanges_rank0"] > 0
+    s = d["strong"]
+    assert s["value"] > 0 and s["config"]["grid"] == [8192, 8192] and s["roofline"]["achieved"] > 0
 
 
 def test_reference_arm_line():
@@ -50,24 +82,3 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "configs[3]" in d["config"]["workload"]
-
-
-def test_bench_two_ranks_under_torchrun():
-    """The driver's N > 1 launch (torchrun, one process per rank) of the
-    weak-scaling line: 16384 rows per rank, row slabs with halo exchange.
-    Both ranks share this box's one GPU, so the exchange runs over gloo
-    (host-staged halos; RD_BENCH_BACKEND) -- a functional check of the
-    N > 1 code path and its JSON line, not a measurement."""
-    env = dict(os.environ, RD_BENCH_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--timesteps", "8", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
-           "--no-cpu-baseline"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
-    assert out.returncode == 0, out.stderr[-3000:]
-    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
-    assert len(lines) == 1, out.stdout[-2000:]  # rank 0 alone prints
-    d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["steps"] == 3
-    assert "configs[4]" in d["config"]["workload"]
-    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
