@@ -337,7 +337,9 @@ int exchange_rows(rd_sim* s, cudaStream_t st) {
 
 // One block of k steps with its halo exchange overlapped with the interior
 // rows (header comment, step 2).
-int dist_block(rd_sim* s, int64_t k) {
+// check: the block's launches run the health check (the block precedes a
+// stamp or the flag read), else the lean tb_kernel variant.
+int dist_block(rd_sim* s, int64_t k, bool check) {
   DistState* d = s->dist;
   s->ghost_valid = (int32_t)s->halo;
   const uint32_t e = ++d->epoch;
@@ -358,7 +360,12 @@ int dist_block(rd_sim* s, int64_t k) {
         return rc;
   }
   RD_CUDA(s, cudaEventRecord(d->ev_start, s->stream));
-  if (plain && a < b && (rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, a, b))) return rc;
+  s->lean_launch = !check;
+  if (plain && a < b && (rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, a, b))) {
+    s->lean_launch = false;
+    return rc;
+  }
+  s->lean_launch = false;
   {
     // the exchange and every wait on another rank live on the exchange
     // stream; the compute stream only waits for its event below
@@ -401,12 +408,15 @@ int dist_block(rd_sim* s, int64_t k) {
   if (!plain) return run_range(s, s->step + k, s->K);
   int32_t lo, hi;
   block_rows(s, (int)k, &lo, &hi);
+  s->lean_launch = !check;
   if (a < b) {
-    if (lo < a && (rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, lo, a))) return rc;
-    if (b < hi && (rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, b, hi))) return rc;
-  } else if ((rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, lo, hi))) {
-    return rc;
+    if (lo < a) rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, lo, a);
+    if (rc == RD_OK && b < hi) rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, b, hi);
+  } else {
+    rc = launch_rows(s, (int)k, s->cur, s->cur ^ 1, lo, hi);
   }
+  s->lean_launch = false;
+  if (rc) return rc;
   if ((rc = end_block(s, (int)k, lo, hi))) return rc;
   s->step += k;
   if (!s->defer_samples && probe_due(s, s->step)) return launch_probes(s, s->step);
@@ -416,8 +426,12 @@ int dist_block(rd_sim* s, int64_t k) {
 int dist_run(rd_sim* s, int64_t n) {
   if (int rc = sync_probes(s)) return rc;
   const int64_t end = s->step + n;
-  while (s->step < end)
-    if (int rc = dist_block(s, std::min<int64_t>(s->halo, end - s->step))) return rc;
+  while (s->step < end) {
+    const int64_t k = std::min<int64_t>(s->halo, end - s->step);
+    bool check = s->step + k >= end;  // the last block before the flag read
+    for (const auto& ev : s->events) check = check || ev.at == s->step + k;  // ... or before a stamp
+    if (int rc = dist_block(s, k, check)) return rc;
+  }
   return RD_OK;
 }
 

@@ -13,14 +13,15 @@ namespace rdl {
 // lp: the level-parallel variant (K <= 4; CTAs of 32*K threads), else
 // tb_kernel (one-warp CTAs). An unsupported combination returns
 // cudaErrorInvalidValue.
-int occupancy_tb_f32(int K, int mode, bool react, bool lp);  // resident CTAs per SM (>= 1)
-int occupancy_tb_f64(int K, int mode, bool react, bool lp);
-inline int occupancy_tb(bool f32, int K, int mode, bool react, bool lp) {
-  return f32 ? occupancy_tb_f32(K, mode, react, lp) : occupancy_tb_f64(K, mode, react, lp);
+// var: rdk::TB_FULL / TB_LEAN / TB_CHECKED (tb_kernel variants).
+int occupancy_tb_f32(int K, int mode, bool react, bool lp, int var);  // resident CTAs per SM (>= 1)
+int occupancy_tb_f64(int K, int mode, bool react, bool lp, int var);
+inline int occupancy_tb(bool f32, int K, int mode, bool react, bool lp, int var) {
+  return f32 ? occupancy_tb_f32(K, mode, react, lp, var) : occupancy_tb_f64(K, mode, react, lp, var);
 }
-cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, unsigned grid,
+cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, int var, unsigned grid,
                       cudaStream_t st);
-cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react, bool lp, unsigned grid,
+cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react, bool lp, int var, unsigned grid,
                       cudaStream_t st);
 
 // cr_kernel over `batch` clusters of cs CTAs with `smem` dynamic shared memory

@@ -2,9 +2,11 @@
 #include "rd_launch_tb.cuh"
 
 namespace rdl {
-cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, unsigned grid,
+cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, int var, unsigned grid,
                       cudaStream_t st) {
-  return detail::dispatch<float>(a, K, mode, react, lp, grid, st, nullptr);
+  return detail::dispatch<float>(a, K, mode, react, lp, var, grid, st, nullptr);
 }
-int occupancy_tb_f32(int K, int mode, bool react, bool lp) { return detail::occupancy<float>(K, mode, react, lp); }
+int occupancy_tb_f32(int K, int mode, bool react, bool lp, int var) {
+  return detail::occupancy<float>(K, mode, react, lp, var);
+}
 }  // namespace rdl

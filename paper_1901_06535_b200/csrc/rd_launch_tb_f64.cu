@@ -2,9 +2,11 @@
 #include "rd_launch_tb.cuh"
 
 namespace rdl {
-cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react, bool lp, unsigned grid,
+cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react, bool lp, int var, unsigned grid,
                       cudaStream_t st) {
-  return detail::dispatch<double>(a, K, mode, react, lp, grid, st, nullptr);
+  return detail::dispatch<double>(a, K, mode, react, lp, var, grid, st, nullptr);
 }
-int occupancy_tb_f64(int K, int mode, bool react, bool lp) { return detail::occupancy<double>(K, mode, react, lp); }
+int occupancy_tb_f64(int K, int mode, bool react, bool lp, int var) {
+  return detail::occupancy<double>(K, mode, react, lp, var);
+}
 }  // namespace rdl

@@ -135,6 +135,7 @@ struct rd_sim {
   int* d_precise = nullptr;
   bool precise_mode = false;
   bool defer_samples = false;  // replay: probes / timelapse sampled only after the step's fault check
+  bool lean_launch = false;    // the next stencil launch may skip its health check (tb_kernel TB_LEAN)
   int* d_flag = nullptr;
   void* d_scratch = nullptr;  // probe max output
   int num_sms = 148;
@@ -394,11 +395,22 @@ cudaError_t launch_stencil(rd_sim* s, int k, int in, int out, int32_t out_lo, in
   rdk::TBArgs<T> a;
   fill_args<T>(s, a, in, out, out_lo, out_hi, k);
   a.n_strips = (int32_t)((s->W + wo - 1) / wo);
-  const int64_t ctas = (int64_t)s->num_sms * rdl::occupancy_tb(sizeof(T) == 4, k, mode, react, lp);
+  // tb_kernel variant: timelapse samples, peer pushes and
+  // PRECISE launches run the full kernel; otherwise the health check runs on
+  // the launches that precede a stamp or the flag read (TB_CHECKED) and no
+  // other (TB_LEAN). RD_TB_VARIANT=full forces the full kernel (A/B runs).
+  static const bool force_full = [] {
+    const char* e = getenv("RD_TB_VARIANT");
+    return e && std::string(e) == "full";
+  }();
+  int var = rdk::TB_FULL;
+  if (mode != rdk::MODE_PRECISE && !a.tl && !s->push_active && !force_full)
+    var = s->lean_launch ? rdk::TB_LEAN : rdk::TB_CHECKED;
+  const int64_t ctas = (int64_t)s->num_sms * rdl::occupancy_tb(sizeof(T) == 4, k, mode, react, lp, var);
   // lp: a task costs ~hb + 3K rows
   a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, lp ? k + (k + 1) / 2 : k, ctas);
   const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
-  return rdl::launch_tb(a, k, mode, react, lp, (unsigned)std::min<int64_t>(tasks, ctas), s->stream);
+  return rdl::launch_tb(a, k, mode, react, lp, var, (unsigned)std::min<int64_t>(tasks, ctas), s->stream);
 }
 
 // One stencil launch of k steps from buffer `in` to `out` producing rows
@@ -793,7 +805,10 @@ int run_blocks(rd_sim* s, int64_t next, int kmax) {
   if (!graph) {
     while (s->step < next) {
       const int k = (int)std::min<int64_t>(kmax, next - s->step);
-      if (int rc = launch_tb(s, k)) return rc;
+      s->lean_launch = s->step + k < next;  // the segment's last launch checks
+      const int rc = launch_tb(s, k);
+      s->lean_launch = false;
+      if (rc) return rc;
       s->step += k;
     }
     return RD_OK;
@@ -806,7 +821,10 @@ int run_blocks(rd_sim* s, int64_t next, int kmax) {
     // segment would not repay the capture)
     while (s->step < next) {
       const int k = (int)std::min<int64_t>(kmax, next - s->step);
-      if (int rc = launch_tb(s, k)) return rc;
+      s->lean_launch = s->step + k < next;  // the segment's last launch checks
+      const int rc = launch_tb(s, k);
+      s->lean_launch = false;
+      if (rc) return rc;
       s->step += k;
     }
     return RD_OK;
@@ -824,7 +842,9 @@ int run_blocks(rd_sim* s, int64_t next, int kmax) {
     if (cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) rc = RD_ECUDA;
     while (rc == RD_OK && s->step < next) {
       const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      s->lean_launch = s->step + k < next;  // the segment's last launch checks
       rc = launch_tb(s, k);
+      s->lean_launch = false;
       s->step += k;
     }
     cudaError_t ec = cudaStreamEndCapture(s->stream, &g);
