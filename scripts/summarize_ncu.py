@@ -82,6 +82,9 @@ def main():
     ap.add_argument("--cr", default=os.path.join(ROOT, "gpurun_out", "prof_cr.ncu-rep"),
                     help="--set full capture of cr_kernel (config 2)")
     ap.add_argument("--cmd", default="")
+    ap.add_argument("--workload", default="c4_roofline", help="bench workload tag of the --full capture")
+    ap.add_argument("--kernel-tag", default="tb_kernel<float,K=4>", help="bench.py's kernel name")
+    ap.add_argument("--cells", type=float, default=16384.0 * 16384 * 4, help="cell-updates per captured launch")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if os.path.exists(a.launches):
@@ -96,14 +99,19 @@ def main():
         json.dump(F, open(os.path.join(PROF, f"{a.round}_tb_kernel_full.json"), "w"), indent=1)
         rb = float(F["dram__bytes_read.sum"]["value"]) * (1e9 if F["dram__bytes_read.sum"]["unit"] == "Gbyte" else 1e6 if F["dram__bytes_read.sum"]["unit"] == "Mbyte" else 1)
         wb = float(F["dram__bytes_write.sum"]["value"]) * (1e9 if F["dram__bytes_write.sum"]["unit"] == "Gbyte" else 1e6 if F["dram__bytes_write.sum"]["unit"] == "Mbyte" else 1)
-        json.dump({"kernel": F["kernel"], "dram_bytes_per_launch": rb + wb, "read": rb, "write": wb,
-                   "source": f"ncu --set full capture ({os.path.basename(a.full)})"},
+        # bench.py uses an entry only for this exact workload / kernel / launch size
+        ent = {"workload": a.workload, "kernel": a.kernel_tag, "cell_updates_per_launch": a.cells,
+               "dram_bytes_per_launch": rb + wb, "read": rb, "write": wb, "ncu_kernel": F["kernel"],
+               "source": f"ncu --set full capture ({os.path.basename(a.full)}), profiles/{a.round}_tb_kernel_full.json"}
+        json.dump({"what": "DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from one ncu "
+                           "--set full capture, with the workload, kernel and cell-updates per launch it was "
+                           "measured on", "entries": [ent]},
                   open(os.path.join(PROF, f"traffic_{a.round}.json"), "w"), indent=1)
         for k, v in F.items():
             print(k, v)
     if os.path.exists(a.cr):
         F = full(a.cr)
-        F["source"] = f"ncu --set full capture ({os.path.basename(a.cr)}), config 2 fp32"
+        F["source"] = f"ncu --set full capture ({os.path.basename(a.cr)}), config 3 fp32 (scripts/gpu_round2_base.sh)"
         json.dump(F, open(os.path.join(PROF, f"{a.round}_cr_kernel_full.json"), "w"), indent=1)
         print("cr_kernel:", {k: F[k] for k in ("gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in F})
 
