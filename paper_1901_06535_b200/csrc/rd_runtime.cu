@@ -61,9 +61,10 @@ struct DistState;  // rd_dist.cuh
 }  // namespace
 
 struct rd_sim {
-  // tb_kernel input maps, one per input buffer (u[i], v[i], phi at a constant
+  // tb_kernel input maps, one per input buffer (u[i], v[i] at a constant
   // stride; see alloc_planes)
   CUtensorMap tmap[2];
+  CUtensorMap tmap_phi;  // phi rows (box: 3 rows), shared by both buffers
   void* arena = nullptr;  // the plane allocation (u, v, phi, checkpoint, push flags)
   size_t arena_bytes = 0;
   bool own_arena = true;     // false: caller-owned (rd_create_device)
@@ -354,6 +355,7 @@ void fill_args(rd_sim* s, rdk::TBArgs<T>& a, int in, int out, int32_t out_lo, in
     for (int64_t b = 0; b < s->B; ++b) a.k[b] = make_consts<T>(s->pinst[b]);
   }
   a.tmap = s->tmap[in];
+  a.tmap_phi = s->tmap_phi;
   a.tm_col0 = (int32_t)s->col_off;
   a.tm_row0 = (int32_t)s->row_off;
   a.fault_key = s->d_fault;
@@ -989,10 +991,10 @@ int restore_checkpoint(rd_sim* s) {
 }
 
 // One allocation of seven plane blocks (a block = the plane of all B
-// instances): u0 | ck_u | u1 | v0 | v1 | ck_v | phi. Then u0, v0, phi sit at
-// a stride of 3 blocks and u1, v1, phi at a stride of 2, so one tensor map per
-// input buffer (dims col, row, instance, plane) lands a row's u, v and phi
-// segments with one TMA (tb_kernel). The checkpoint fills the two gaps.
+// instances): u0 | ck_u | u1 | v0 | v1 | ck_v | phi. Then u0, v0 sit at a
+// stride of 3 blocks and u1, v1 at a stride of 2, so one tensor map per input
+// buffer (dims col, row, instance, plane) lands three rows' u and v segments
+// with one TMA (tb_kernel). The checkpoint fills the two gaps.
 size_t arena_size(const rd_sim* s) { return 7 * (size_t)s->B * s->plane_stride * s->esz + 256; }
 
 int alloc_planes(rd_sim* s, void* ext, size_t ext_bytes) {
@@ -1028,25 +1030,33 @@ int alloc_planes(rd_sim* s, void* ext, size_t ext_bytes) {
 }
 
 // The tensor maps of tb_kernel's input rows (driver entry point through the
-// runtime: no libcuda link). Box = one row segment of 32*V columns of the
-// three planes; coordinates are relative to the plane's allocation start.
+// runtime: no libcuda link), coordinates relative to the plane's allocation
+// start: per input buffer one 4-D map whose box is three rows of 32*V
+// columns of the u and v planes; one 3-D map whose box is three rows of phi.
 int encode_tmaps(rd_sim* s) {
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(driver_entry("cuTensorMapEncodeTiled"));
   if (!encode) return set_err(s, RD_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const cuuint64_t block = (cuuint64_t)s->B * s->plane_stride * s->esz;
   const cuuint32_t seg = (cuuint32_t)(32 * (16 / s->esz));
+  const auto dtype = s->esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
   for (int i = 0; i < 2; ++i) {
-    const cuuint64_t dims[4] = {(cuuint64_t)s->pitch, (cuuint64_t)s->rows_alloc, (cuuint64_t)s->B, 3};
+    const cuuint64_t dims[4] = {(cuuint64_t)s->pitch, (cuuint64_t)s->rows_alloc, (cuuint64_t)s->B, 2};
     const cuuint64_t strides[3] = {(cuuint64_t)(s->pitch * s->esz), (cuuint64_t)(s->plane_stride * s->esz),
                                    (i == 0 ? 3 : 2) * block};
-    const cuuint32_t box[4] = {seg, 1, 1, 3};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = encode(&s->tmap[i], s->esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                        4, s->u[i], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    const cuuint32_t box[4] = {seg, 3, 1, 2};
+    CUresult r = encode(&s->tmap[i], dtype, 4, s->u[i], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(s, RD_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   }
+  const cuuint64_t dims[3] = {(cuuint64_t)s->pitch, (cuuint64_t)s->rows_alloc, (cuuint64_t)s->B};
+  const cuuint64_t strides[2] = {(cuuint64_t)(s->pitch * s->esz), (cuuint64_t)(s->plane_stride * s->esz)};
+  const cuuint32_t box[3] = {seg, 3, 1};
+  CUresult r = encode(&s->tmap_phi, dtype, 3, s->phi, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(s, RD_ECUDA, "cuTensorMapEncodeTiled (phi) failed (%d)", (int)r);
   return RD_OK;
 }
 
