@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         newest = max(_mtime(p) for p in [src, *deps, __file__])
         if force or _mtime(obj) < newest:
-            cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src]
+            # RD_NVCC_DEFS: extra -D flags for A/B builds of kernel variants
+            cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("RD_NVCC_DEFS", "").split(), "-c", "-o", obj, src]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             procs.append((subprocess.Popen(cmd), cmd, obj))
