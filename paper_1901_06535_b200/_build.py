@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "librd.so")
 OBJDIR = os.path.join(HERE, "build")
 CSRC = os.path.join(HERE, "csrc")
 RD_H = os.path.join(ROOT, "include", "rd.h")
-KERNELS = [os.path.join(CSRC, f) for f in ("rd_kernels.cuh", "rd_launch.h")]
+KERNELS = [os.path.join(CSRC, f) for f in ("rd_kernels.cuh", "rd_launch.h", "rd_gz.cuh")]
 # the runtime and the kernel-instantiation units (rd_launch.h), compiled in
 # parallel and linked into one shared library: source -> headers it includes
 UNITS = {
@@ -24,6 +24,7 @@ UNITS = {
     "rd_launch_tb_f32.cu": KERNELS + [os.path.join(CSRC, "rd_launch_tb.cuh")],
     "rd_launch_tb_f64.cu": KERNELS + [os.path.join(CSRC, "rd_launch_tb.cuh")],
     "rd_launch_cr.cu": KERNELS,
+    "rd_launch_gz.cu": KERNELS,
 }
 SOURCES = [os.path.join(CSRC, f) for f in UNITS]
 

@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "rd_gz.cuh"
 #include "rd_kernels.cuh"
 
 namespace rdl {
@@ -31,5 +32,13 @@ cudaError_t launch_cr(const rdk::CrArgs<float>& a, int mode, bool react, bool pa
                       size_t smem, cudaStream_t st, bool query, int* clusters);
 cudaError_t launch_cr(const rdk::CrArgs<double>& a, int mode, bool react, bool pal, int cs, unsigned batch,
                       size_t smem, cudaStream_t st, bool query, int* clusters);
+
+// gz_kernel over `grid` tiles (cooperative launch: all resident) with
+// `smem` dynamic shared memory, m zone vectors per thread; occ: return the
+// resident CTAs per SM in *occ instead of launching.
+cudaError_t launch_gz(const rdk::GzArgs<float>& a, int mode, bool react, int m, unsigned grid, size_t smem,
+                      cudaStream_t st, int* occ);
+cudaError_t launch_gz(const rdk::GzArgs<double>& a, int mode, bool react, int m, unsigned grid, size_t smem,
+                      cudaStream_t st, int* occ);
 
 }  // namespace rdl

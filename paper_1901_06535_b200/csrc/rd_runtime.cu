@@ -84,7 +84,15 @@ struct rd_sim {
   int cr_cs = 0;        // CTAs per cluster for cr_kernel
   size_t cr_smem = 0;   // its dynamic shared memory per CTA
   bool cr_pal = false;  // cr_kernel with phi as palette indices
-  bool margins_stale = false;   // u/v mirror margins not refreshed since a cr_kernel launch
+  // a8 whole-chip tiles (gz_kernel): tile geometry, exchange planes, epochs
+  bool use_gz = false;
+  struct GzGeom {
+    int k = 0, gx = 0, th = 0, tw = 0, tr = 0, tc = 0, nr = 0, nv = 0, m = 0;
+    size_t smem = 0;
+  } gz;
+  void* gz_x = nullptr;   // LL exchange planes [parity][u, v] (8-byte words, 1 per fp32 / 2 per fp64 cell)
+  unsigned gz_epoch = 0;  // the next launch's exchanges carry gz_epoch + 1, + 2, ...
+  bool margins_stale = false;   // u/v mirror margins not refreshed since a cr_kernel / gz_kernel launch
   int64_t probes_done_at = -1;  // the step whose probes a cr_kernel launch evaluated
   std::vector<std::vector<double>> pal;  // distinct phi values per instance (cr PAL layout)
   bool pal_ok = true;     // every instance has <= 256
@@ -678,6 +686,176 @@ int launch_cr(rd_sim* s, int64_t n) {
   return RD_OK;
 }
 
+// ---- a8 whole-chip tiles (gz_kernel, rd_gz.cuh) ------------------------------
+// The probe schedule of a fused launch of n steps: gcd of the strides of the
+// probes due at some step in (step, step + n], and the steps to its first
+// multiple.
+void fused_probe_schedule(const rd_sim* s, int64_t n, int32_t* every, int32_t* first) {
+  int64_t g = 0;
+  for (const auto& q : s->probes)
+    if (q.stride > 0 && (s->step + n) / q.stride > s->step / q.stride) g = std::gcd(g, (int64_t)q.stride);
+  *every = (int32_t)g;
+  *first = g ? (int32_t)(g - s->step % g) : 0;
+}
+
+template <typename T>
+cudaError_t launch_gz_t(rd_sim* s, int64_t n, const rd_sim::GzGeom& z, unsigned grid, bool query, int* occ) {
+  rdk::GzArgs<T> ga;
+  std::memset(&ga, 0, sizeof ga);
+  if (!query) {
+    fill_args<T>(s, ga.a, s->cur, s->cur ^ 1, 0, (int32_t)s->H, (int)n);
+    const int64_t lw = s->esz == 4 ? 1 : 2;  // LL words per cell
+    const int64_t words = s->B * s->plane_stride * lw, org = (s->row_off * s->pitch + s->col_off) * lw;
+    auto* x = static_cast<unsigned long long*>(s->gz_x);
+    for (int par = 0; par < 2; ++par)
+      for (int f = 0; f < 2; ++f) ga.x[par][f] = x + (2 * par + f) * words + org;
+    ga.epoch0 = s->gz_epoch;
+    ga.k = z.k;
+    ga.gx = z.gx;
+    ga.th = z.th;
+    ga.tw = z.tw;
+    ga.tr = z.tr;
+    ga.tc = z.tc;
+    ga.nr = z.nr;
+    ga.nv = z.nv;
+    ga.n = (int32_t)n;
+    ga.n_probes = (int32_t)s->probes.size();
+    ga.probes = s->d_probes;
+    ga.first_fire = s->d_first;
+    ga.step0 = s->step;
+    fused_probe_schedule(s, n, &ga.probe_every, &ga.probe_first);
+    ga.timeout_ns = 2000000000ull;  // 2 s: only a broken launch waits this long
+  }
+  const bool react = !(s->g.flags & RD_REACTION_OFF);
+  return rdl::launch_gz(ga, react ? s->fast_mode : rdk::MODE_PRECISE, react, z.m, grid, z.smem, s->stream,
+                        query ? occ : nullptr);
+}
+
+cudaError_t gz_dispatch(rd_sim* s, int64_t n, const rd_sim::GzGeom& z, unsigned grid, bool query, int* occ) {
+  return s->esz == 4 ? launch_gz_t<float>(s, n, z, grid, query, occ) : launch_gz_t<double>(s, n, z, grid, query, occ);
+}
+
+// Tile geometry of gz_kernel for block depth k: the tiling (rows x columns
+// of tiles per instance, tile widths a multiple of V) whose busiest SM has
+// the least work per step -- the vectors of its tile's computed region,
+// averaged over the k steps of a block (the owned region grown by k - s),
+// times the tiles it holds -- among those with at most `capacity` tiles,
+// tiles at least k rows and gx columns (a tile's ghost zone lies inside its
+// neighbours' border rings), at most kGzMaxSlots zone vectors per thread and
+// the shared arrays within `smem_max`.
+bool gz_geometry(const rd_sim* s, int k, int capacity, size_t smem_max, rd_sim::GzGeom* out) {
+  const int V = 16 / (int)s->esz;
+  const int gx = (k + V - 1) / V * V;
+  double best = 0;
+  bool found = false;
+  for (int64_t tr = 1; tr <= s->H / k; ++tr) {
+    const int64_t th = (s->H + tr - 1) / tr;
+    if ((s->H + th - 1) / th != tr || th < k) continue;  // the same tiling as a smaller tr
+    for (int64_t tc = 1; tc <= (s->W + V - 1) / V; ++tc) {
+      const int64_t tw = ((s->W + tc - 1) / tc + V - 1) / V * V;
+      if ((s->W + tw - 1) / tw != tc || tw < gx) continue;
+      const int64_t tiles = s->B * tr * tc;
+      if (tiles > capacity) continue;
+      const int64_t nr = th + 2 * k, nv = (tw + 2 * gx) / V;
+      if (nr * nv > (int64_t)rdk::kGzThreads * rdk::kGzMaxSlots || nr >= 65536) continue;
+      const size_t smem = rdk::gz_smem_bytes((int)nr, (int)nv, V, (int)s->esz);
+      if (smem > smem_max) continue;
+      const double work = (double)(th + k) * (double)((tw + k + V - 1) / V + 1) *
+                          std::ceil((double)tiles / (double)s->num_sms);
+      if (!found || work < best - 1e-9) {
+        found = true;
+        best = work;
+        out->k = k;
+        out->gx = gx;
+        out->th = (int)th;
+        out->tw = (int)tw;
+        out->tr = (int)tr;
+        out->tc = (int)tc;
+        out->nr = (int)nr;
+        out->nv = (int)nv;
+        out->m = (int)((nr * nv + rdk::kGzThreads - 1) / rdk::kGzThreads);
+        out->smem = smem;
+      }
+    }
+  }
+  return found;
+}
+
+// Decide whether small instances run as whole-chip tiles (gz_kernel); fast
+// modes and single-GPU handles only, like cr_kernel. RD_GZ_K overrides the
+// block depth (steps per exchange).
+void choose_gz(rd_sim* s, bool forced) {
+  s->use_gz = false;
+  if (s->slab || s->fast_mode == rdk::MODE_PRECISE) return;
+  const char* ek = getenv("RD_GZ_K");
+  const int k = ek ? std::max(1, atoi(ek)) : 8;
+  const int V = 16 / (int)s->esz;
+  const int gx = (k + V - 1) / V * V;
+  if (s->H < 2 * k || s->W < 2 * gx + V) return;  // mirrored ghosts stay inside the grid
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return;
+  rd_sim::GzGeom z;
+  if (!gz_geometry(s, k, s->num_sms, (size_t)optin - 64, &z)) return;
+  int occ = 0;
+  if (gz_dispatch(s, 0, z, 0, true, &occ) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const int64_t tiles = s->B * z.tr * z.tc;
+  if (occ < 1 || tiles > (int64_t)occ * s->num_sms) return;
+  (void)forced;
+  // LL exchange planes: [parity][u, v], zeroed (epoch 0 = nothing published)
+  if (!s->gz_x) {
+    const size_t bytes = (size_t)4 * s->B * s->plane_stride * (s->esz == 4 ? 1 : 2) * 8;
+    if (cudaMalloc(&s->gz_x, bytes) != cudaSuccess || cudaMemsetAsync(s->gz_x, 0, bytes, s->stream) != cudaSuccess) {
+      cudaGetLastError();
+      if (s->gz_x) cudaFree(s->gz_x);
+      s->gz_x = nullptr;
+      return;
+    }
+    s->gz_epoch = 0;
+  }
+  s->gz = z;
+  s->use_gz = true;
+}
+
+bool gz_runs(const rd_sim* s) {
+  return s->use_gz && !s->precise_mode && !(s->g.flags & RD_NO_CHECKPOINT);
+}
+
+// One whole-chip tiled launch of n steps: reads buffer cur, writes cur ^ 1.
+// It evaluates the probes due at any of its steps and leaves the global mirror
+// margins stale (like cr_kernel).
+int launch_gz(rd_sim* s, int64_t n) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (s->profiling) {
+    if (s->ev_used == s->ev_pool.size()) {
+      cudaEvent_t a, b;
+      RD_CUDA(s, cudaEventCreate(&a));
+      RD_CUDA(s, cudaEventCreate(&b));
+      s->ev_pool.push_back({a, b});
+    }
+    e0 = s->ev_pool[s->ev_used].first;
+    e1 = s->ev_pool[s->ev_used].second;
+    ++s->ev_used;
+    RD_CUDA(s, cudaEventRecord(e0, s->stream));
+  }
+  const unsigned grid = (unsigned)(s->B * s->gz.tr * s->gz.tc);
+  cudaError_t e = gz_dispatch(s, n, s->gz, grid, false, nullptr);
+  if (e != cudaSuccess) return set_err(s, RD_ECUDA, "gz_kernel launch: %s", cudaGetErrorString(e));
+  if (s->profiling) RD_CUDA(s, cudaEventRecord(e1, s->stream));
+  s->gz_epoch += (unsigned)((n + s->gz.k - 1) / s->gz.k);
+  s->cur ^= 1;
+  s->margins_stale = true;
+  if (!s->probes.empty() && probe_due(s, s->step + n)) s->probes_done_at = s->step + n;
+  s->st.launches++;
+  s->st.step_launches++;
+  s->st.cell_updates += s->B * s->H * s->W * n;
+  return RD_OK;
+}
+
 // Bounding box of a shape in global rows / columns, clipped to the grid.
 void shape_bbox(const rdk::ShapeDev& sh, int64_t Hg, int64_t W, int64_t* i0, int64_t* i1, int64_t* j0,
                 int64_t* j1) {
@@ -796,6 +974,11 @@ bool probe_due(const rd_sim* s, int64_t step) {
 // launches per block (the per-launch overhead dominates small batched grids).
 int run_blocks(rd_sim* s, int64_t next, int kmax) {
   Range r_("rd_step.segment");
+  if (gz_runs(s) && next > s->step) {
+    if (int rc = launch_gz(s, next - s->step)) return rc;
+    s->step = next;
+    return RD_OK;
+  }
   if (cr_runs(s) && next > s->step) {
     if (int rc = launch_cr(s, next - s->step)) return rc;
     s->step = next;
@@ -904,7 +1087,7 @@ int run_range(rd_sim* s, int64_t end, int kmax) {
     int64_t next = end;
     for (const auto& ev : s->events)
       if (ev.at > s->step) next = std::min(next, ev.at);
-    if (!cr_runs(s))  // cr_kernel latches the probes due inside its segment
+    if (!cr_runs(s) && !gz_runs(s))  // cr_kernel / gz_kernel latch the probes due inside their segment
       for (const auto& q : s->probes)
         if (q.stride > 0) next = std::min(next, (s->step / q.stride + 1) * (int64_t)q.stride);
     if (s->tl_stride > 0) next = std::min(next, (s->step / s->tl_stride + 1) * (int64_t)s->tl_stride);
@@ -1129,6 +1312,8 @@ void select_kernels(rd_sim* s) {
   const std::string want = e ? e : "auto";
   s->use_lp = want == "lp";
   s->use_cr = false;
+  s->use_gz = false;
+  if (want == "gz") choose_gz(s, true);
   if (want == "auto" || want == "cr") choose_cr(s, want == "cr");
 }
 
@@ -1441,8 +1626,8 @@ int rd_destroy(rd_sim* s) {
   if (s->dist) dist_destroy(s);
   for (void* m : s->ipc_mapped) cudaIpcCloseMemHandle(m);
   if (s->arena && s->own_arena) cudaFree(s->arena);
-  void* ps[] = {s->tl,    s->ck_tl,  s->d_probes, s->d_first, s->d_first_ck,
-                s->d_fault, s->d_flag, s->d_scratch, s->d_idx, s->d_pal, s->d_pal_n};
+  void* ps[] = {s->tl,        s->ck_tl,   s->d_probes, s->d_first, s->d_first_ck, s->d_fault,
+                s->d_flag,    s->d_scratch, s->d_idx,  s->d_pal,   s->d_pal_n,    s->gz_x};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& e : s->ev_pool) {
@@ -2037,7 +2222,9 @@ int rd_get_stats(rd_sim* s, rd_stats* out) {
   out->timed_launches = s->acc_timed;
   out->tb_depth = s->K;
   out->arith_mode = (s->g.flags & RD_NO_CHECKPOINT) ? rdk::MODE_PRECISE : s->fast_mode;
-  out->kernel = (s->use_cr && !(s->g.flags & RD_NO_CHECKPOINT)) ? 2 : (s->use_lp ? 1 : 0);
+  out->kernel = (s->use_gz && !(s->g.flags & RD_NO_CHECKPOINT))
+                    ? 3
+                    : ((s->use_cr && !(s->g.flags & RD_NO_CHECKPOINT)) ? 2 : (s->use_lp ? 1 : 0));
   return RD_OK;
 }
 

@@ -72,7 +72,7 @@ def run(n, dtype, tb):
     roof = hbm_gbs() / (20 if np.dtype(dtype).itemsize == 4 else 40)
     return {"config": w.name, "dtype": np.dtype(dtype).name, "B": w.B, "H": w.H, "W": w.W, "steps": w.steps,
             "device_ms": ms, "wall_s": wall, "gcell_updates_per_s": gcells,
-            "frac_of_one_step_hbm_roofline": gcells / roof, "stencil_kernel": ["tb", "lp", "cr"][st["kernel"]],
+            "frac_of_one_step_hbm_roofline": gcells / roof, "stencil_kernel": ["tb", "lp", "cr", "gz"][st["kernel"]],
             "launches": st["launches"], "step_launches": st["step_launches"], "tb_depth": st["tb_depth"],
             "first_fire": fires, "expect": w.expect.get("fires")}
 

@@ -22,11 +22,12 @@ def table1():
     return golden("table1_params.json")
 
 
-@pytest.fixture(params=["tb", "lp", "cr"])
+@pytest.fixture(params=["tb", "lp", "cr", "gz"])
 def kernel(request, monkeypatch):
     """Run a GPU test with each stencil kernel: the register-pipelined
-    tb_kernel, the level-parallel lp_kernel and the cluster-resident cr_kernel
-    (RD_KERNEL, read at rd_create; cr applies where the instance fits shared
-    memory, else the handle falls back to tb_kernel)."""
+    tb_kernel, the level-parallel lp_kernel, the cluster-resident cr_kernel
+    and the whole-chip tiled gz_kernel (RD_KERNEL, read at rd_create; cr / gz
+    apply where the instance fits their limits, else the handle falls back to
+    tb_kernel)."""
     monkeypatch.setenv("RD_KERNEL", request.param)
     return request.param

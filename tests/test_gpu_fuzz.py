@@ -76,7 +76,7 @@ def _case(seed):
         splits.append(n)
         left -= n
     return dict(dt=dt, B=B, H=H, W=W, steps=steps, phis=phis, inits=inits, evs=evs, prs=prs, params=params,
-                tb=int(g.integers(0, 9)), kernel=str(g.choice(["auto", "tb", "lp", "cr"])),
+                tb=int(g.integers(0, 9)), kernel=str(g.choice(["auto", "tb", "lp", "cr", "gz"])),
                 tl=int(g.choice([0, 0, 1, 5, 13])), splits=splits)
 
 
@@ -84,6 +84,7 @@ def _case(seed):
 def test_randomized_parity(seed, monkeypatch):
     c = _case(seed)
     monkeypatch.setenv("RD_KERNEL", c["kernel"])
+    monkeypatch.setenv("RD_GZ_K", str(1 + seed % 12))  # gz_kernel: steps per border exchange
     dt = c["dt"]
     sim = rd.Sim(np.stack(c["phis"]), dtype=dt, tb_depth=c["tb"])
     try:
