@@ -408,7 +408,7 @@ def per_config(cpu_seconds: float):
             e = {"config": f"configs[{n - 1}] {w.name}", "dtype": np.dtype(dt).name, "batch": w.B,
                  "grid": [w.H, w.W], "time_steps": w.steps, "device_ms": ms,
                  "gcell_updates_per_s": cells / (ms / 1e3) / 1e9,
-                 "stencil_kernel": ["tb_kernel", "lp_kernel", "cr_kernel"][st["kernel"]],
+                 "stencil_kernel": ["tb_kernel", "lp_kernel", "cr_kernel", "gz_kernel"][st["kernel"]],
                  "kernel_launches": st["launches"], "first_fire": fires, "fires": got, "expected_fires": exp,
                  "outcome_ok": (got == exp) if exp is not None else None}
             if cpu_seconds > 0:

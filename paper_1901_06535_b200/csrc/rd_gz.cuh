@@ -39,7 +39,14 @@
 
 namespace rdk {
 
-constexpr int kGzThreads = 512;
+#ifdef RD_GZ_PROF
+// measurement build only: per-CTA cycle counts of the phases of a block
+// (compute, publish, first fetch pass, remaining wait, barrier), summed over
+// launches; read with rd_gz_prof_dump (rd_runtime.cu)
+__device__ unsigned long long g_gz_prof[2048 * 8];
+#endif
+
+constexpr int kGzThreads = 512;  // threads of a one-tile-per-SM CTA; 256 when two tiles share an SM
 constexpr int kGzMaxSlots = 6;  // zone vectors per thread
 
 template <typename T>
@@ -56,6 +63,7 @@ struct GzArgs {
   int32_t tr, tc;   // tiles per instance (rows x columns)
   int32_t nr, nv;   // tile array: rows (th + 2k) and vectors per row ((tw + 2 gx) / V)
   int32_t n;        // steps in this launch
+  int32_t nt;       // threads per tile (kernel instantiation): 512 or 256
   int32_t n_probes;
   const ProbeDev* probes;  // a6 fused: latched probes
   long long* first_fire;
@@ -140,6 +148,9 @@ __device__ __forceinline__ bool ll_fetch(const unsigned long long* xu, const uns
     bool ok = true;
 #pragma unroll
     for (int i = 0; i < V * LW; ++i) ok = ok && (unsigned)(wu[i] >> 32) == ep && (unsigned)(wv[i] >> 32) == ep;
+#ifdef RD_GZ_TIMING_NO_WAIT  // measurement build only: results are wrong
+    ok = true;
+#endif
     if (ok) break;
     if (gz_now() > deadline) return false;
   }
@@ -180,16 +191,18 @@ __device__ __forceinline__ void gz_probes(const GzArgs<T>& ga, int b, int row0, 
   }
 }
 
-// shared memory of a tile array of nr rows x nv vectors: u ping-pong and phi
-// (rows padded by a vector on each side) and the layer-sorted vector list
+// shared memory of a tile array of nr rows x nv vectors: u ping-pong, phi and
+// the exchange's v staging plane (rows padded by a vector on each side), and
+// the layer-sorted vector list
 __host__ __device__ constexpr size_t gz_smem_bytes(int nr, int nv, int V, int esz) {
-  return (size_t)3 * nr * (nv + 2) * V * esz + (size_t)nr * nv * 4;
+  return (size_t)4 * nr * (nv + 2) * V * esz + (size_t)nr * nv * 4;
 }
 
-template <typename T, bool REACT, int MODE, int M, bool PROBE>
-__global__ void __launch_bounds__(kGzThreads, 1) gz_kernel(const __grid_constant__ GzArgs<T> ga) {
+// NT threads per tile: 512 (one tile per SM) or 256 (two tiles per SM, so
+// one tile computes while the other waits for its neighbours' words)
+template <typename T, bool REACT, int MODE, int M, bool PROBE, int NT>
+__global__ void __launch_bounds__(NT, kGzThreads / NT) gz_kernel(const __grid_constant__ GzArgs<T> ga) {
   constexpr int V = 16 / (int)sizeof(T);
-  constexpr int NT = kGzThreads;
   constexpr int LW = LL<T>::W;
   const TBArgs<T>& a = ga.a;
   const int ntile = ga.tr * ga.tc;
@@ -210,7 +223,8 @@ __global__ void __launch_bounds__(kGzThreads, 1) gz_kernel(const __grid_constant
   T* U0 = reinterpret_cast<T*>(gz_smem);
   T* U1 = U0 + plane;
   T* Ps = U1 + plane;
-  uint32_t* list = reinterpret_cast<uint32_t*>(Ps + plane);
+  T* Vx = Ps + plane;  // staging of the ghost zone's v at an exchange
+  uint32_t* list = reinterpret_cast<uint32_t*>(Vx + plane);
   __shared__ int abort_flag;
   __shared__ int warp_tot[NT / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -302,8 +316,16 @@ __global__ void __launch_bounds__(kGzThreads, 1) gz_kernel(const __grid_constant
   float minb = INFINITY;
   int p = 0;  // U[p] holds the latest step
   int to_probe = ga.probe_first;
+#ifdef RD_GZ_PROF
+  __shared__ unsigned long long pf_blockmax;
+  unsigned long long pf_c = 0, pf_pub = 0, pf_bar = 0, pf_n = 0, pf_f = 0;
+#endif
   for (int s0 = 0, blk = 0; s0 < ga.n; s0 += k, ++blk) {
     const int kb = min(k, ga.n - s0);
+#ifdef RD_GZ_PROF
+    const unsigned long long pf0 = clock64();
+    if (t == 0) pf_blockmax = 0;
+#endif
     for (int s = 1; s <= kb; ++s) {
       const unsigned lmax = (unsigned)(k - s);  // active: layer <= k - s
       const T* src = p ? U1 : U0;
@@ -341,8 +363,16 @@ __global__ void __launch_bounds__(kGzThreads, 1) gz_kernel(const __grid_constant
       }
     }
     if (s0 + kb >= ga.n) break;
+#ifdef RD_GZ_TIMING_NO_EXCHANGE  // measurement build only: results are wrong
+    continue;
+#endif
     // ---- exchange (parity blk & 1): publish the owned border ring as LL
     // words, then poll the ghost zone's words and reload them
+#ifdef RD_GZ_PROF
+    const unsigned long long pf1 = clock64();
+    pf_c += pf1 - pf0;
+    ++pf_n;
+#endif
     const unsigned ep = ga.epoch0 + (unsigned)blk + 1u;
     unsigned long long* xu = ga.x[blk & 1][0] + inst * LW;
     unsigned long long* xv = ga.x[blk & 1][1] + inst * LW;
@@ -355,32 +385,101 @@ __global__ void __launch_bounds__(kGzThreads, 1) gz_kernel(const __grid_constant
       ll_put<T, V>(xu, wi, u[m], ep);
       ll_put<T, V>(xv, wi, v[m], ep);
     }
+#ifdef RD_GZ_PROF
+    const unsigned long long pf2 = clock64();
+    pf_pub += pf2 - pf1;
+#endif
     {
-      const unsigned long long deadline = gz_now() + ga.timeout_ns;
+      // the ghost zone cell by cell over the whole CTA (all of a thread's
+      // words requested before any is checked: one L2 round trip when the
+      // neighbours are done; words not yet published are re-polled): u into
+      // the current buffer, v into the staging plane; then every thread
+      // takes its ghost slots from shared memory
       T* cur = p ? U1 : U0;
+      const unsigned long long deadline = gz_now() + ga.timeout_ns;
+      const int gw = jz1 - (jo1 - jo0);        // ghost cells of an owned row
+      const int n_top = xo0 * jz1;             // cells of the ghost rows above
+      const int n_mid = (xo1 - xo0) * gw;      // ghost cells beside the owned rows
+      const int n_all = n_top + n_mid + k * jz1;  // + the ghost rows below
+      constexpr int G = 4;  // cells per thread in flight
       bool ok = true;
+      for (int c0 = 0; ok && c0 < n_all; c0 += NT * G) {
+        unsigned long long wu[G][LW], wv[G][LW];
+        int off[G];
+        int64_t wi[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int c = c0 + t + NT * g;
+          int x, j;
+          if (c < n_top) {
+            x = c / jz1, j = c - x * jz1;
+          } else if (c < n_top + n_mid) {
+            const int r = (c - n_top) / gw, q = c - n_top - r * gw;
+            x = xo0 + r, j = q < jo0 ? q : jo1 + (q - jo0);
+          } else {
+            const int r = (c - n_top - n_mid) / jz1;
+            x = xo1 + r, j = c - n_top - n_mid - r * jz1;
+          }
+          off[g] = c < n_all ? x * PW + V + j : -1;
+          wi[g] = ((int64_t)gz_refl(row0 + x, H) * pitch + gz_refl(col0 + j, W)) * LW;
+        }
+        unsigned pending = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) pending |= (unsigned)(off[g] >= 0) << g;
+        while (pending) {
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int h = 0; h < LW; ++h)
+              if ((pending >> g) & 1u) {
+                wu[g][h] = ll_ld(xu + wi[g] + h);
+                wv[g][h] = ll_ld(xv + wi[g] + h);
+              }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            if (!((pending >> g) & 1u)) continue;
+            bool r = true;
+#pragma unroll
+            for (int h = 0; h < LW; ++h) r = r && (unsigned)(wu[g][h] >> 32) == ep && (unsigned)(wv[g][h] >> 32) == ep;
+#ifdef RD_GZ_TIMING_NO_WAIT  // measurement build only: results are wrong
+            r = true;
+#endif
+            if (r) {
+              cur[off[g]] = LL<T>::unpack(wu[g]);
+              Vx[off[g]] = LL<T>::unpack(wv[g]);
+              pending &= ~(1u << g);
+            }
+          }
+          if (pending && gz_now() > deadline) {
+            ok = false;
+            break;
+          }
+        }
+      }
+      if (!ok) atomicExch(&abort_flag, 1);
+      __syncthreads();
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const unsigned L = lf[m] & 0xffu;
-        if (!ok || L == 0xffu || (L == 0 && !(lf[m] & 0x400u))) continue;  // unused, or owned and current
-        const int x = o[m] / PW, j0 = o[m] % PW - V;
-        const int64_t wrow = (int64_t)gz_refl(row0 + x, H) * pitch;
-        const bool orow = x >= xo0 && x < xo1;
-        int64_t wi[V];
-        unsigned need = 0;
+        if (L == 0xffu || (L == 0 && !(lf[m] & 0x400u))) continue;  // unused, or owned and current
+        const int j0 = o[m] % PW - V;
 #pragma unroll
         for (int e = 0; e < V; ++e) {
-          const int j = j0 + e;
-          // owned lane of a vector straddling W; columns past the zone are never needed
-          need |= (unsigned)(!((orow && j >= jo0 && j < jo1) || j >= jz1)) << e;
-          wi[e] = (wrow + gz_refl(col0 + j, W)) * LW;
+          if (L == 0 && j0 + e < jo1) continue;  // owned lane of a vector straddling W
+          u[m][e] = cur[o[m] + e];
+          v[m][e] = Vx[o[m] + e];
         }
-        ok = ll_fetch<T, V>(xu, xv, wi, need, ep, u[m], v[m], deadline);
-        *reinterpret_cast<int4*>(cur + o[m]) = *reinterpret_cast<const int4*>(u[m]);
       }
-      if (!ok) atomicExch(&abort_flag, 1);
     }
+#ifdef RD_GZ_PROF
+    const unsigned long long pf3 = clock64();
+    atomicMax(&pf_blockmax, pf3 - pf2);  // the slowest thread's fetch (first pass + waits)
+#endif
     __syncthreads();
+#ifdef RD_GZ_PROF
+    pf_bar += clock64() - pf3;
+    pf_f += pf_blockmax;
+#endif
     if (abort_flag) break;
   }
 
@@ -407,6 +506,16 @@ __global__ void __launch_bounds__(kGzThreads, 1) gz_kernel(const __grid_constant
     }
   }
   if (MODE != MODE_PRECISE && ((REACT && minb < kFastDivMinB) || bad || abort_flag)) *a.precise_flag = 1;
+#ifdef RD_GZ_PROF
+  if (t == 0 && blockIdx.x < 2048) {
+    unsigned long long* q = g_gz_prof + blockIdx.x * 8;
+    atomicAdd(q + 0, pf_c);
+    atomicAdd(q + 1, pf_pub);
+    atomicAdd(q + 2, pf_f);
+    atomicAdd(q + 3, pf_bar);
+    atomicAdd(q + 4, pf_n);
+  }
+#endif
 }
 
 }  // namespace rdk

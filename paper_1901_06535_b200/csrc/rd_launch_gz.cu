@@ -5,15 +5,21 @@
 namespace rdl {
 namespace {
 
-template <typename T, bool REACT, int MODE, int M, bool PROBE>
-cudaError_t go(const rdk::GzArgs<T>& ga, unsigned grid, size_t smem, cudaStream_t st, int* occ) {
-  auto fn = rdk::gz_kernel<T, REACT, MODE, M, PROBE>;
+template <typename T, bool REACT, int MODE, int M, bool PROBE, int NT>
+cudaError_t go_nt(const rdk::GzArgs<T>& ga, unsigned grid, size_t smem, cudaStream_t st, int* occ) {
+  auto fn = rdk::gz_kernel<T, REACT, MODE, M, PROBE, NT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, rdk::kGzThreads, smem);
+  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, NT, smem);
   // cooperative: every tile resident at once (tiles wait on their neighbours)
   void* args[] = {const_cast<rdk::GzArgs<T>*>(&ga)};
-  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(rdk::kGzThreads), args, smem, st);
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(NT), args, smem, st);
+}
+
+template <typename T, bool REACT, int MODE, int M, bool PROBE>
+cudaError_t go(const rdk::GzArgs<T>& ga, unsigned grid, size_t smem, cudaStream_t st, int* occ) {
+  return ga.nt == 256 ? go_nt<T, REACT, MODE, M, PROBE, 256>(ga, grid, smem, st, occ)
+                      : go_nt<T, REACT, MODE, M, PROBE, rdk::kGzThreads>(ga, grid, smem, st, occ);
 }
 
 template <typename T, bool REACT, int MODE, int M>
@@ -62,3 +68,13 @@ cudaError_t launch_gz(const rdk::GzArgs<double>& a, int mode, bool react, int m,
 }
 
 }  // namespace rdl
+
+#ifdef RD_GZ_PROF
+// measurement build only: copy (and clear) the per-CTA phase cycle counts
+extern "C" int rd_gz_prof_dump(unsigned long long* out, int n) {
+  if (n > 2048 * 8) n = 2048 * 8;
+  if (cudaMemcpyFromSymbol(out, rdk::g_gz_prof, n * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  static unsigned long long zero[2048 * 8];
+  return cudaMemcpyToSymbol(rdk::g_gz_prof, zero, sizeof zero) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -87,7 +87,7 @@ struct rd_sim {
   // a8 whole-chip tiles (gz_kernel): tile geometry, exchange planes, epochs
   bool use_gz = false;
   struct GzGeom {
-    int k = 0, gx = 0, th = 0, tw = 0, tr = 0, tc = 0, nr = 0, nv = 0, m = 0;
+    int k = 0, gx = 0, th = 0, tw = 0, tr = 0, tc = 0, nr = 0, nv = 0, m = 0, nt = 0;
     size_t smem = 0;
   } gz;
   void* gz_x = nullptr;   // LL exchange planes [parity][u, v] (8-byte words, 1 per fp32 / 2 per fp64 cell)
@@ -542,14 +542,17 @@ cudaError_t cr_dispatch(rd_sim* s, bool pal, int64_t n, size_t smem, int cs, boo
 // pipeline-latency floor or, above it, the whole batch spread over the chip.
 // fp64 cr bands are ALU-latency bound (DFMA chains), so large fp64 batches of
 // a few instances stay on tb_kernel, which uses every SM.
-bool cr_beats_tb(const rd_sim* s, int cs) {
+double t_cr_step(const rd_sim* s, int cs) {
   const bool f32 = s->esz == 4;
   const double band = (double)((s->H + cs - 1) / cs) * (double)s->W;
-  const double total = (double)s->B * (double)s->H * (double)s->W;
-  const double t_cr = (f32 ? 0.38e-6 : 0.31e-6) + band * (f32 ? 0.19e-9 : 0.50e-9);
-  const double t_tb = std::max(f32 ? 3.0e-6 : 3.3e-6, total * (f32 ? 7.9e-12 : 8.9e-12));  // fp64: depth 5
-  return t_cr < t_tb;
+  return (f32 ? 0.38e-6 : 0.31e-6) + band * (f32 ? 0.19e-9 : 0.50e-9);
 }
+double t_tb_step(const rd_sim* s) {
+  const bool f32 = s->esz == 4;
+  const double total = (double)s->B * (double)s->H * (double)s->W;
+  return std::max(f32 ? 3.0e-6 : 3.3e-6, total * (f32 ? 7.9e-12 : 8.9e-12));  // fp64: depth 5
+}
+bool cr_beats_tb(const rd_sim* s, int cs) { return t_cr_step(s, cs) < t_tb_step(s); }
 
 // Decide whether small instances run cluster-resident: the largest cluster
 // (16, 8, 4, 2 CTAs) whose per-CTA band fits in shared memory -- with phi as
@@ -702,6 +705,7 @@ template <typename T>
 cudaError_t launch_gz_t(rd_sim* s, int64_t n, const rd_sim::GzGeom& z, unsigned grid, bool query, int* occ) {
   rdk::GzArgs<T> ga;
   std::memset(&ga, 0, sizeof ga);
+  ga.nt = z.nt;
   if (!query) {
     fill_args<T>(s, ga.a, s->cur, s->cur ^ 1, 0, (int32_t)s->H, (int)n);
     const int64_t lw = s->esz == 4 ? 1 : 2;  // LL words per cell
@@ -735,69 +739,105 @@ cudaError_t gz_dispatch(rd_sim* s, int64_t n, const rd_sim::GzGeom& z, unsigned 
   return s->esz == 4 ? launch_gz_t<float>(s, n, z, grid, query, occ) : launch_gz_t<double>(s, n, z, grid, query, occ);
 }
 
-// Tile geometry of gz_kernel for block depth k: the tiling (rows x columns
-// of tiles per instance, tile widths a multiple of V) whose busiest SM has
-// the least work per step -- the vectors of its tile's computed region,
-// averaged over the k steps of a block (the owned region grown by k - s),
-// times the tiles it holds -- among those with at most `capacity` tiles,
-// tiles at least k rows and gx columns (a tile's ghost zone lies inside its
-// neighbours' border rings), at most kGzMaxSlots zone vectors per thread and
-// the shared arrays within `smem_max`.
-bool gz_geometry(const rd_sim* s, int k, int capacity, size_t smem_max, rd_sim::GzGeom* out) {
+// Tile geometry of gz_kernel for block depth k: tiles per instance (rows x
+// columns, tile widths a multiple of V) and one or two tiles per SM (512 or
+// 256 threads). Per-step time model, fitted on B200 (configs 2-3, fp32 and
+// fp64): a tile computes the vectors of its owned region
+// grown by k - s at step s -- on average (th + k) x ((tw + k) / V + 1) --
+// at kGzVecNs per vector on its SM, and waits kGzExchangeUs per exchange
+// (every k steps) for its neighbours; two tiles on one SM share its issue
+// slots but hide each other's exchange wait. Constraints: at most the
+// resident tiles, tiles at least k rows and gx columns (a tile's ghost zone
+// lies inside its neighbours' border rings), at most kGzMaxSlots zone
+// vectors per thread, the shared arrays within the SM's share.
+// The exchange of a block of k steps costs kGzExchangeUs[0] plus
+// kGzExchangeUs[1] per step of ghost depth and 4 bytes of cell (its ring
+// and zone grow with k; fp64 LL words are twice the fp32 ones).
+constexpr double kGzVecNs = 0.7, kGzExchangeUs[2] = {1.2, 0.2};
+// returns the predicted seconds per step (0: no geometry)
+double gz_geometry(const rd_sim* s, int k, size_t smem_max, rd_sim::GzGeom* out) {
   const int V = 16 / (int)s->esz;
   const int gx = (k + V - 1) / V * V;
+  // tiles per SM: 1 (two tiles per SM measured slower on configs 1-3,
+  // DESIGN.md §5.2d); RD_GZ_TPS=2 (or 0: the model's choice) for measurements
+  const char* etps = getenv("RD_GZ_TPS");
+  const int only_tps = etps ? atoi(etps) : 1;
   double best = 0;
   bool found = false;
-  for (int64_t tr = 1; tr <= s->H / k; ++tr) {
-    const int64_t th = (s->H + tr - 1) / tr;
-    if ((s->H + th - 1) / th != tr || th < k) continue;  // the same tiling as a smaller tr
-    for (int64_t tc = 1; tc <= (s->W + V - 1) / V; ++tc) {
-      const int64_t tw = ((s->W + tc - 1) / tc + V - 1) / V * V;
-      if ((s->W + tw - 1) / tw != tc || tw < gx) continue;
-      const int64_t tiles = s->B * tr * tc;
-      if (tiles > capacity) continue;
-      const int64_t nr = th + 2 * k, nv = (tw + 2 * gx) / V;
-      if (nr * nv > (int64_t)rdk::kGzThreads * rdk::kGzMaxSlots || nr >= 65536) continue;
-      const size_t smem = rdk::gz_smem_bytes((int)nr, (int)nv, V, (int)s->esz);
-      if (smem > smem_max) continue;
-      const double work = (double)(th + k) * (double)((tw + k + V - 1) / V + 1) *
-                          std::ceil((double)tiles / (double)s->num_sms);
-      if (!found || work < best - 1e-9) {
-        found = true;
-        best = work;
-        out->k = k;
-        out->gx = gx;
-        out->th = (int)th;
-        out->tw = (int)tw;
-        out->tr = (int)tr;
-        out->tc = (int)tc;
-        out->nr = (int)nr;
-        out->nv = (int)nv;
-        out->m = (int)((nr * nv + rdk::kGzThreads - 1) / rdk::kGzThreads);
-        out->smem = smem;
+  for (int tps : {1, 2}) {
+    if (only_tps && tps != only_tps) continue;
+    const int nt = rdk::kGzThreads / tps;
+    const int64_t capacity = (int64_t)tps * s->num_sms;
+    for (int64_t tr = 1; tr <= s->H / k; ++tr) {
+      const int64_t th = (s->H + tr - 1) / tr;
+      if ((s->H + th - 1) / th != tr || th < k) continue;  // the same tiling as a smaller tr
+      for (int64_t tc = 1; tc <= (s->W + V - 1) / V; ++tc) {
+        const int64_t tw = ((s->W + tc - 1) / tc + V - 1) / V * V;
+        if ((s->W + tw - 1) / tw != tc || tw < gx) continue;
+        const int64_t tiles = s->B * tr * tc;
+        if (tiles > capacity) continue;
+        const int64_t nr = th + 2 * k, nv = (tw + 2 * gx) / V;
+        if (nr * nv > (int64_t)nt * rdk::kGzMaxSlots || nr >= 65536) continue;
+        const size_t smem = rdk::gz_smem_bytes((int)nr, (int)nv, V, (int)s->esz);
+        if (smem * tps > smem_max) continue;
+        const double work = (double)(th + k) * (double)((tw + k + V - 1) / V + 1) * kGzVecNs * 1e-9;
+        const double x = (kGzExchangeUs[0] + kGzExchangeUs[1] * k * (double)s->esz / 4.0) * 1e-6 / k;
+        const int per_sm = (int)((tiles + s->num_sms - 1) / s->num_sms);  // tiles sharing the busiest SM
+        const double t = per_sm > 1 ? std::max(per_sm * work, work + x) : work + x;
+        if (!found || t < best * (1 - 1e-9)) {
+          found = true;
+          best = t;
+          out->k = k;
+          out->gx = gx;
+          out->th = (int)th;
+          out->tw = (int)tw;
+          out->tr = (int)tr;
+          out->tc = (int)tc;
+          out->nr = (int)nr;
+          out->nv = (int)nv;
+          out->m = (int)((nr * nv + nt - 1) / nt);
+          out->nt = nt;
+          out->smem = smem;
+        }
       }
     }
   }
-  return found;
+  return found ? best : 0.0;
 }
 
 // Decide whether small instances run as whole-chip tiles (gz_kernel); fast
 // modes and single-GPU handles only, like cr_kernel. RD_GZ_K overrides the
 // block depth (steps per exchange).
-void choose_gz(rd_sim* s, bool forced) {
+// forced: RD_KERNEL=gz; otherwise only when the model predicts less time per
+// step than t_other (the cr / tb alternative). RD_GZ_K fixes the block depth
+// (steps per exchange); by default the model picks it from 4..12.
+void choose_gz(rd_sim* s, bool forced, double t_other) {
   s->use_gz = false;
   if (s->slab || s->fast_mode == rdk::MODE_PRECISE) return;
-  const char* ek = getenv("RD_GZ_K");
-  const int k = ek ? std::max(1, atoi(ek)) : 8;
-  const int V = 16 / (int)s->esz;
-  const int gx = (k + V - 1) / V * V;
-  if (s->H < 2 * k || s->W < 2 * gx + V) return;  // mirrored ghosts stay inside the grid
-  int dev = 0, optin = 0;
+  int dev = 0, optin = 0, smem_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess)
     return;
+  const size_t smem_max = (size_t)std::min(optin, smem_sm - 2048) - 64;
+  const char* ek = getenv("RD_GZ_K");
+  const int V = 16 / (int)s->esz;
   rd_sim::GzGeom z;
-  if (!gz_geometry(s, k, s->num_sms, (size_t)optin - 64, &z)) return;
+  double best = 0;
+  for (int k : {4, 5, 6, 8, 10, 12}) {
+    if (ek) k = std::max(1, atoi(ek));
+    const int gx = (k + V - 1) / V * V;
+    rd_sim::GzGeom zk;
+    double t = 0;
+    if (s->H >= 2 * k && s->W >= 2 * gx + V)  // mirrored ghosts stay inside the grid
+      t = gz_geometry(s, k, smem_max, &zk);
+    if (t > 0 && (best == 0 || t < best)) {
+      best = t;
+      z = zk;
+    }
+    if (ek) break;
+  }
+  if (best == 0 || (!forced && best >= t_other)) return;
   int occ = 0;
   if (gz_dispatch(s, 0, z, 0, true, &occ) != cudaSuccess) {
     cudaGetLastError();
@@ -805,7 +845,6 @@ void choose_gz(rd_sim* s, bool forced) {
   }
   const int64_t tiles = s->B * z.tr * z.tc;
   if (occ < 1 || tiles > (int64_t)occ * s->num_sms) return;
-  (void)forced;
   // LL exchange planes: [parity][u, v], zeroed (epoch 0 = nothing published)
   if (!s->gz_x) {
     const size_t bytes = (size_t)4 * s->B * s->plane_stride * (s->esz == 4 ? 1 : 2) * 8;
@@ -1304,17 +1343,25 @@ bool foldable(const rd_params& p) {
 // Arithmetic mode for the handle's parameter set(s): FOLD when every 1/dx^2
 // is a power of two, FOLD_DIV4 when additionally (fp32, reaction on) the
 // 4-op division is certified for every q; else PRECISE.
-// Stencil kernel choice: cr_kernel for small instances that fit one wave of
-// clusters, else tb_kernel. RD_KERNEL=tb|lp|cr forces one (tests,
-// measurements; cr still needs the instance to fit shared memory).
+// Stencil kernel choice: gz_kernel or cr_kernel for small instances (whichever
+// the per-step models predict faster, each only where it fits), else
+// tb_kernel. RD_KERNEL=tb|lp|cr|gz forces one (tests, measurements; cr and gz
+// still need the instance to fit their limits, else tb_kernel runs).
 void select_kernels(rd_sim* s) {
   const char* e = getenv("RD_KERNEL");
   const std::string want = e ? e : "auto";
   s->use_lp = want == "lp";
   s->use_cr = false;
   s->use_gz = false;
-  if (want == "gz") choose_gz(s, true);
+  if (want == "gz") choose_gz(s, true, 0.0);
   if (want == "auto" || want == "cr") choose_cr(s, want == "cr");
+  if (want == "auto") {
+    // whole-chip tiles when their model beats the cluster-resident or the
+    // streaming kernel
+    const double t_other = s->use_cr ? t_cr_step(s, s->cr_cs) : t_tb_step(s);
+    choose_gz(s, false, t_other);
+    if (s->use_gz) s->use_cr = false;
+  }
 }
 
 int choose_mode(rd_sim* s) {

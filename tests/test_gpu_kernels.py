@@ -56,10 +56,8 @@ def test_certified_four_op_division_selected_for_table1_q():
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_cluster_resident_kernel_selection_and_parity(dtype, monkeypatch):
-    """a8: instances that fit a cluster's shared memory run on cr_kernel by
-    default (rd_stats.kernel == 2) when its cost model predicts a gain --
-    configs 1-3 in fp32, configs 1-2 in fp64 (config 2 with phi as palette
-    indices) --
+    """a8: configs 1-3 run on gz_kernel by default (rd_stats.kernel == 3);
+    cr_kernel (forced) on instances that fit a cluster's shared memory is
     bitwise equal to the oracle and to tb_kernel, over row splits with and
     without a ragged remainder (H % cs != 0), narrow W (< one block of
     threads) and a segment cut by a mid-run stimulus."""
@@ -69,13 +67,13 @@ def test_cluster_resident_kernel_selection_and_parity(dtype, monkeypatch):
     from rdinputs import config, noise_plane
     dt = np.float32 if dtype == "f32" else np.float64
     monkeypatch.delenv("RD_KERNEL", raising=False)
-    # fp64 config 3: the cost model keeps it on tb_kernel (all SMs) -- forced
-    # cr is covered below
-    fits = {1: True, 2: True, 3: dt == np.float32}
-    for n, want in fits.items():
+    # the default choice on configs 1-3 is now gz_kernel (whole-chip tiles,
+    # its model beats cr_kernel's on every one); cr_kernel
+    # is forced below
+    for n in (1, 2, 3):
         w = config(n, dtype=dt)
         sim = rd.Sim(np.stack([w.phi_plane(b).astype(dt) for b in range(w.B)]), dtype=dt)
-        assert sim.stats()["kernel"] == (2 if want else 0), n
+        assert sim.stats()["kernel"] == 3, n
         sim.close()
     for (H, W) in [(64, 64), (37, 131), (301, 29), (9, 700), (150, 150)]:
         u0 = noise_plane(H, W, 0, seed=4, dtype=dt)
