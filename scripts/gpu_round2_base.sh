@@ -1,6 +1,6 @@
 # Round-2 baseline on the current HEAD: the GPU suite, the default bench line,
 # the reference arm, the ncu launch list of the bench command and one --set full
-# capture of tb_kernel (config 4) and cr_kernel (config 3 fp32).
+# capture of tb_kernel (config 4) and gz_kernel (config 3 fp32).
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv,noheader > gpurun_out/gpu.txt
 timeout 1500 python -m pytest tests -x -q -m gpu -p no:cacheprovider > gpurun_out/t_all.log 2>&1; echo tests rc=$?; tail -3 gpurun_out/t_all.log
@@ -16,5 +16,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tb_k
 echo "full rc=$?"
 CMD3="python scripts/bench_configs.py --configs 3 --dtype f32 --repeat 1"
 timeout 300 $CMD3 > gpurun_out/plain_cr.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:cr_kernel -s 0 -c 1 -o gpurun_out/prof_cr $CMD3 > gpurun_out/ncu_cr.log 2>&1
-echo "cr rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gz_kernel -s 0 -c 1 -o gpurun_out/prof_gz $CMD3 > gpurun_out/ncu_gz.log 2>&1
+echo "gz rc=$?"
+timeout 600 python scripts/bench_configs.py --configs 1,2,3 --repeat 2 > gpurun_out/bench_configs.log 2>&1; echo "configs rc=$?"

@@ -81,6 +81,8 @@ def main():
     ap.add_argument("--full", default=os.path.join(ROOT, "gpurun_out", "prof_full.ncu-rep"))
     ap.add_argument("--cr", default=os.path.join(ROOT, "gpurun_out", "prof_cr.ncu-rep"),
                     help="--set full capture of cr_kernel (config 2)")
+    ap.add_argument("--gz", default=os.path.join(ROOT, "gpurun_out", "prof_gz.ncu-rep"),
+                    help="--set full capture of gz_kernel (config 3 fp32)")
     ap.add_argument("--cmd", default="")
     ap.add_argument("--workload", default="c4_roofline", help="bench workload tag of the --full capture")
     ap.add_argument("--kernel-tag", default="tb_kernel<float,K=4>", help="bench.py's kernel name")
@@ -114,6 +116,15 @@ def main():
         F["source"] = f"ncu --set full capture ({os.path.basename(a.cr)}), config 3 fp32 (scripts/gpu_round2_base.sh)"
         json.dump(F, open(os.path.join(PROF, f"{a.round}_cr_kernel_full.json"), "w"), indent=1)
         print("cr_kernel:", {k: F[k] for k in ("gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in F})
+    gz_summary(a)
+
+
+def gz_summary(a):
+    if os.path.exists(a.gz):
+        F = full(a.gz)
+        F["source"] = f"ncu --set full capture ({os.path.basename(a.gz)}), config 3 fp32 (2 x 200x600, 20000 steps)"
+        json.dump(F, open(os.path.join(PROF, f"{a.round}_gz_kernel_full.json"), "w"), indent=1)
+        print("gz_kernel:", {k: F[k] for k in ("gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in F})
 
 
 if __name__ == "__main__":
