@@ -317,14 +317,14 @@ __global__ void __launch_bounds__(NT, kGzThreads / NT) gz_kernel(const __grid_co
   int p = 0;  // U[p] holds the latest step
   int to_probe = ga.probe_first;
 #ifdef RD_GZ_PROF
-  __shared__ unsigned long long pf_blockmax;
-  unsigned long long pf_c = 0, pf_pub = 0, pf_bar = 0, pf_n = 0, pf_f = 0;
+  __shared__ unsigned long long pf_blockmax, pf_passmax, pf_loadmax;
+  unsigned long long pf_c = 0, pf_pub = 0, pf_bar = 0, pf_n = 0, pf_f = 0, pf_p = 0, pf_l = 0;
 #endif
   for (int s0 = 0, blk = 0; s0 < ga.n; s0 += k, ++blk) {
     const int kb = min(k, ga.n - s0);
 #ifdef RD_GZ_PROF
     const unsigned long long pf0 = clock64();
-    if (t == 0) pf_blockmax = 0;
+    if (t == 0) pf_blockmax = pf_passmax = pf_loadmax = 0;
 #endif
     for (int s = 1; s <= kb; ++s) {
       const unsigned lmax = (unsigned)(k - s);  // active: layer <= k - s
@@ -397,6 +397,10 @@ __global__ void __launch_bounds__(NT, kGzThreads / NT) gz_kernel(const __grid_co
       // takes its ghost slots from shared memory
       T* cur = p ? U1 : U0;
       const unsigned long long deadline = gz_now() + ga.timeout_ns;
+#ifdef RD_GZ_PROF
+      unsigned long long pf_passes = 0;
+      const unsigned long long pf_f0 = clock64();
+#endif
       const int gw = jz1 - (jo1 - jo0);        // ghost cells of an owned row
       const int n_top = xo0 * jz1;             // cells of the ghost rows above
       const int n_mid = (xo1 - xo0) * gw;      // ghost cells beside the owned rows
@@ -427,6 +431,9 @@ __global__ void __launch_bounds__(NT, kGzThreads / NT) gz_kernel(const __grid_co
 #pragma unroll
         for (int g = 0; g < G; ++g) pending |= (unsigned)(off[g] >= 0) << g;
         while (pending) {
+#ifdef RD_GZ_PROF
+          ++pf_passes;
+#endif
 #pragma unroll
           for (int g = 0; g < G; ++g)
 #pragma unroll
@@ -457,6 +464,10 @@ __global__ void __launch_bounds__(NT, kGzThreads / NT) gz_kernel(const __grid_co
         }
       }
       if (!ok) atomicExch(&abort_flag, 1);
+#ifdef RD_GZ_PROF
+      atomicMax(&pf_passmax, pf_passes);
+      atomicMax(&pf_loadmax, clock64() - pf_f0);
+#endif
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < M; ++m) {
@@ -479,6 +490,8 @@ __global__ void __launch_bounds__(NT, kGzThreads / NT) gz_kernel(const __grid_co
 #ifdef RD_GZ_PROF
     pf_bar += clock64() - pf3;
     pf_f += pf_blockmax;
+    pf_p += pf_passmax;
+    pf_l += pf_loadmax;
 #endif
     if (abort_flag) break;
   }
@@ -514,6 +527,8 @@ __global__ void __launch_bounds__(NT, kGzThreads / NT) gz_kernel(const __grid_co
     atomicAdd(q + 2, pf_f);
     atomicAdd(q + 3, pf_bar);
     atomicAdd(q + 4, pf_n);
+    atomicAdd(q + 5, pf_p);
+    atomicAdd(q + 6, pf_l);
   }
 #endif
 }

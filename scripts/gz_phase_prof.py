@@ -36,8 +36,9 @@ lib.rd_gz_prof_dump(buf, 2048 * 8)
 arr = np.frombuffer(buf, dtype=np.uint64).reshape(2048, 8).astype(np.float64)
 used = arr[:, 4] > 0
 blocks = arr[used, 4]
-ph = arr[used, :4] / blocks[:, None]
+ph = arr[used, :7] / blocks[:, None]
 print(f"{used.sum()} CTAs, {blocks.mean():.0f} exchange blocks each; cycles per block (mean / max over CTAs):")
-for i, name in enumerate(["compute", "publish", "slowest fetch", "post barrier"]):
+for i, name in [(0, "compute"), (1, "publish"), (2, "slowest fetch"), (3, "post barrier"),
+                (5, "poll passes (max thread)"), (6, "fetch loop (max thread)")]:
     print(f"  {name:14s} {ph[:, i].mean():9.0f} {ph[:, i].max():9.0f}")
 sim.close()
