@@ -222,72 +222,45 @@ class ThreadCtx:
 
 # ------------------------------------------------------------- our arm
 
-def e2e_pipelined(rd, sim, w, dtype, tb, pu, pv, T, depth, steps, cells):
-    """e2e with `depth` handles of the same workload, each driven by its own
-    host thread through the public API (ctypes releases the GIL; each handle
-    has its own CUDA stream). Every step still copies its inputs in from
-    pinned host memory and its result out, inside the timed region; one job's
-    copies overlap another job's stencil launches (copy engines vs SMs), and
-    the jobs' stencil launches do not overlap each other (one steps at a time).
-    Timed on the host clock between two device synchronisations."""
+def e2e_pipelined(rd, sim, pu, pv, T, steps, cells):
+    """e2e on ONE handle from ONE host thread with the library's asynchronous
+    host I/O (include/rd.h: rd_write_fields_async / rd_commit_fields /
+    rd_read_fields_async / rd_io_wait). Every step is a job: its inputs are
+    copied in from pinned host memory and its result out to pinned host
+    memory, inside the timed region; job i+1's upload and job i-1's download
+    run on the copy engines while job i's stencil launches own the SMs (the
+    first upload and the last download are exposed). Timed on the host clock
+    between two device synchronisations."""
     import torch
-    sims = [sim] + [rd.Sim(None, shape=(1, w.H, w.W), dtype=dtype, tb_depth=tb)
-                    for _ in range(depth - 1)]
-    try:
-        rd.rd_set_stream(sim.h, 0)  # back to the handle's own stream
-        for s in sims[1:]:
-            s.paint_phi(0.054)
-            for shape, val, at in w.events[0]:
-                s.stimulate(shape, val, at)
-            s.write(0, pu, pv)
-            s.step(T)  # warm-up: events consumed, segment graphs captured
-        outs = [(torch.empty(pu.shape, dtype=torch.float32, pin_memory=True).numpy(),
-                 torch.empty(pu.shape, dtype=torch.float32, pin_memory=True).numpy()) for _ in sims]
-        counts = [steps // depth + (1 if k < steps % depth else 0) for k in range(depth)]
-        errors = []
-        # staggered start: job k begins once job k-1's first inputs are on the
-        # device, so the first launch does not wait for every job's upload
-        uploaded = [threading.Event() for _ in range(depth)]
-        # one job steps at a time (two concurrent stencil grids would share
-        # the SMs and break tb_kernel's one-wave schedule); uploads and
-        # read-backs of the other jobs proceed meanwhile on the copy engines
-        compute = threading.Lock()
-
-        def job(k):
-            try:
-                if k:
-                    uploaded[k - 1].wait()
-                for i in range(counts[k]):
-                    rd.rd_write_fields(sims[k].h, 0, pu, pv)
-                    if i == 0:
-                        uploaded[k].set()
-                    with compute:
-                        sims[k].step(T)
-                    rd.rd_read_fields(sims[k].h, 0, *outs[k])
-            except Exception as e:  # surfaced below
-                errors.append(e)
-            finally:
-                uploaded[k].set()
-
-        threads = [threading.Thread(target=job, args=(k,)) for k in range(depth)]
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        torch.cuda.synchronize()
-        secs = time.perf_counter() - t0
-        if errors:
-            raise errors[0]
-    finally:
-        for s in sims[1:]:
-            s.close()
+    h = sim.h
+    rd.rd_set_stream(h, 0)  # back to the handle's own stream
+    outs = [(torch.empty(pu.shape, dtype=torch.float32, pin_memory=True).numpy(),
+             torch.empty(pu.shape, dtype=torch.float32, pin_memory=True).numpy()) for _ in range(2)]
+    # untimed: allocate the staging blocks, touch every buffer once
+    rd.rd_write_fields_async(h, 0, pu, pv)
+    rd.rd_commit_fields(h)
+    rd.rd_read_fields_async(h, 0, *outs[0])
+    rd.rd_read_fields_async(h, 0, *outs[1])
+    rd.rd_io_wait(h)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rd.rd_write_fields_async(h, 0, pu, pv)
+    rd.rd_commit_fields(h)
+    for i in range(steps):
+        if i + 1 < steps:
+            rd.rd_write_fields_async(h, 0, pu, pv)  # the next job's inputs, under this job's steps
+        sim.step(T)
+        rd.rd_read_fields_async(h, 0, *outs[i % 2])  # snapshot, drained under the next job's steps
+        if i + 1 < steps:
+            rd.rd_commit_fields(h)
+    rd.rd_io_wait(h)
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
     return {"value": cells * T * steps / secs / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": 2 * cells * 4, "d2h_bytes_per_step": 2 * cells * 4, "steps": steps,
-            "pipeline": depth, "timer": "host clock between device synchronisations",
-            "api": f"{depth} handles, one host thread each: rd_write_fields(host pinned) + rd_step + "
-                   "rd_read_fields(host) every step"}
+            "pipeline": 2, "timer": "host clock between device synchronisations",
+            "api": "one handle, one host thread: rd_write_fields_async(host pinned) of the next job + rd_step + "
+                   "rd_read_fields_async(host pinned) + rd_commit_fields, every step; rd_io_wait at the end"}
 
 
 def load_traffic(workload: str, kernel: str, cells_per_launch: float):
@@ -435,6 +408,40 @@ def oracle_rate(w, dt, seconds: float):
             "sample": f"instance 0, first {n} of {w.steps} time steps"}
 
 
+def config4_fp64(T: int = 200):
+    """configs[3]'s grid and inputs in fp64 (north_star: the stencil kernel "in
+    fp32 and fp64"): T time steps of rd_step, device-timed after one warm-up
+    call, with the one-step HBM roofline (40 B per cell-update) beside it."""
+    import torch
+    import paper_1901_06535_b200 as rd
+    from rdinputs import config
+    w = config(4)
+    dt = np.dtype(np.float64)
+    with rd.Sim(None, shape=(1, w.H, w.W), dtype=dt) as sim:
+        sim.paint_phi(0.054)
+        sim.fill_noise(seed=1)
+        for shape, val, at in w.events[0]:
+            sim.stimulate(shape, val, at)
+        stream = torch.cuda.current_stream()
+        sim.set_stream(stream)
+        sim.step(T)
+        rd.rd_reset_stats(sim.h)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        sim.step(T)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        st = sim.stats()
+    hbm, _ = peaks()
+    g = w.H * w.W * T / (ms / 1e3) / 1e9
+    return {"config": "configs[3] c4_roofline grid and inputs, fp64", "dtype": "float64", "grid": [w.H, w.W],
+            "time_steps": T, "device_ms": ms, "gcell_updates_per_s": g, "tb_depth": st["tb_depth"],
+            "stencil_kernel": ["tb_kernel", "lp_kernel", "cr_kernel", "gz_kernel"][st["kernel"]],
+            "frac_of_one_step_hbm_roofline": g / (hbm / BYTES_PER_CELL[dt])}
+
+
 def fp32_error():
     """BASELINE.json north_star's literal fp32 check, reported (reading R-17):
     max |u_fp32 - u_fp64| on config 1 after 300 and 1000 steps, both computed
@@ -513,8 +520,7 @@ def run_single(args):
                "steps": args.e2e_steps, "api": "rd_write_fields(host pinned) + rd_step + rd_read_fields(host)"}
         if args.e2e_pipeline > 1:
             serial = e2e
-            e2e = e2e_pipelined(rd, sim, w, dtype, args.tb, pu, pv, T, args.e2e_pipeline, args.e2e_pipeline_steps,
-                                cells)
+            e2e = e2e_pipelined(rd, sim, pu, pv, T, args.e2e_pipeline_steps, cells)
             e2e["serial"] = {"value": serial["value"], "steps": serial["steps"], "api": serial["api"]}
     launches = st["launches"]
     sim.close()
@@ -529,6 +535,7 @@ def run_single(args):
     if not args.no_configs:
         line["per_config"] = per_config(0 if args.no_cpu_baseline else args.config_cpu_seconds)
         line["fp32_error"] = fp32_error()
+        line["fp64_large"] = config4_fp64()
     return line
 
 
@@ -758,8 +765,9 @@ def main():
     ap.add_argument("--tb", type=int, default=0, help="temporal-blocking depth (0 = auto)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-pipeline", type=int, default=2,
-                    help="handles (host threads) of the pipelined e2e leg at N = 1 (1: serial only)")
-    ap.add_argument("--e2e-pipeline-steps", type=int, default=16)
+                    help="N = 1: 2 = e2e with the library's asynchronous host I/O (copies of the neighbouring jobs "
+                         "under a job's steps), 1 = the serial write/step/read only")
+    ap.add_argument("--e2e-pipeline-steps", type=int, default=24)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",

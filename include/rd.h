@@ -259,6 +259,38 @@ int rd_read_fields(struct rd_sim* sim, int32_t b, void* u_out, void* v_out);
 int rd_read_fields_device(struct rd_sim* sim, int32_t b, void* u_out, void* v_out);
 int rd_write_fields_device(struct rd_sim* sim, int32_t b, const void* u, const void* v);
 
+/* Asynchronous host I/O: the same copies as rd_write_fields / rd_read_fields,
+ * overlapped with rd_step on the copy engines, so that a caller who runs one
+ * job after another on a handle (new fields in, n steps, fields out: the
+ * paper's interactive use, as a batch loop) pays the host
+ * copies only once per pipeline, not once per job. Host buffers should be
+ * pinned (pageable memory works but copies synchronously) and are
+ * [height][width] of dtype, as above. The first call allocates two dense
+ * staging blocks of 2 * batch * height * width elements on the device.
+ *   rd_write_fields_async  start uploading instance b's u and/or v into the
+ *       staging block on the handle's upload stream and return. The handle's
+ *       state is NOT changed; rd_step keeps working on the current fields. The
+ *       host buffers must stay valid until rd_commit_fields or rd_io_wait
+ *       returns.
+ *   rd_commit_fields       wait for the uploads staged so far, check them
+ *       (RD_ENONFINITE: nothing is written and the staged set is dropped) and
+ *       copy them into the current fields, device to device, on the handle's
+ *       stream. Syncs that stream. No staged upload: a no-op.
+ *   rd_read_fields_async   snapshot instance b's current u and/or v into the
+ *       second staging block (device to device, stream-ordered after the
+ *       preceding rd_step) and start copying the snapshot to the host on the
+ *       download stream; returns at once, and a following rd_step or
+ *       rd_commit_fields does not disturb the snapshot. The host buffers hold
+ *       the fields after rd_io_wait returns.
+ *   rd_io_wait             block until every upload and download started so
+ *       far has finished.
+ * Errors: RD_ERANGE (b), RD_ENOMEM (staging blocks), RD_ECUDA, RD_ENONFINITE
+ * (rd_commit_fields). rd_destroy waits for copies in flight. */
+int rd_write_fields_async(struct rd_sim* sim, int32_t b, const void* u, const void* v);
+int rd_commit_fields(struct rd_sim* sim);
+int rd_read_fields_async(struct rd_sim* sim, int32_t b, void* u_out, void* v_out);
+int rd_io_wait(struct rd_sim* sim);
+
 /* ---- stimulation (a1) ---- */
 
 /* Schedule u := value on the shape's cells of instance b (-1 = all) before

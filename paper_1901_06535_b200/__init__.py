@@ -23,7 +23,8 @@ __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
            "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_step_begin", "rd_step_finish", "RD_BLOCK_PUSH", "rd_plane_origins", "rd_set_peer", "rd_push_ghosts", "rd_flag_ptr", "rd_ipc_export", "rd_ipc_map", "rd_stream_signal", "rd_stream_wait", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load", "rd_get_geometry", "rd_arena_bytes", "rd_create_device",
-           "rd_field_ptr", "rd_dist_unique_id", "rd_dist_local_id", "rd_create_dist"]
+           "rd_field_ptr", "rd_dist_unique_id", "rd_dist_local_id", "rd_create_dist", "rd_write_fields_async",
+           "rd_commit_fields", "rd_read_fields_async", "rd_io_wait"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
 _DT = {np.dtype(np.float32): RD_F32, np.dtype(np.float64): RD_F64}
@@ -346,6 +347,27 @@ def rd_read_fields(h, b: int, u_out: np.ndarray | None, v_out: np.ndarray | None
 
 def rd_write_fields(h, b: int, u: np.ndarray | None, v: np.ndarray | None) -> None:
     _check(load().rd_write_fields(h, b, _host(u, h, what="u"), _host(v, h, what="v")), h)
+
+
+def rd_write_fields_async(h, b: int, u: np.ndarray | None, v: np.ndarray | None) -> None:
+    """Start uploading u, v (pinned host arrays the caller keeps alive until
+    rd_commit_fields / rd_io_wait) into the handle's staging block."""
+    _check(load().rd_write_fields_async(h, b, _host(u, h, what="u"), _host(v, h, what="v")), h)
+
+
+def rd_commit_fields(h) -> None:
+    _check(load().rd_commit_fields(h), h)
+
+
+def rd_read_fields_async(h, b: int, u_out: np.ndarray | None, v_out: np.ndarray | None) -> None:
+    """Snapshot the fields and start copying them to u_out, v_out (valid after
+    rd_io_wait; the caller keeps the arrays alive until then)."""
+    _check(load().rd_read_fields_async(h, b, _host(u_out, h, what="u_out", writable=True),
+                                       _host(v_out, h, what="v_out", writable=True)), h)
+
+
+def rd_io_wait(h) -> None:
+    _check(load().rd_io_wait(h), h)
 
 
 def rd_read_fields_device(h, b: int, u_ptr: int | None, v_ptr: int | None) -> None:

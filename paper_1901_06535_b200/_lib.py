@@ -81,6 +81,10 @@ SYMBOLS = [
     ("rd_read_fields", C.c_int, [P, i32, P, P]),
     ("rd_read_fields_device", C.c_int, [P, i32, P, P]),
     ("rd_write_fields_device", C.c_int, [P, i32, P, P]),
+    ("rd_write_fields_async", C.c_int, [P, i32, P, P]),
+    ("rd_commit_fields", C.c_int, [P]),
+    ("rd_read_fields_async", C.c_int, [P, i32, P, P]),
+    ("rd_io_wait", C.c_int, [P]),
     ("rd_stimulate", C.c_int, [P, i32, C.POINTER(rd_shape), dbl, i64]),
     ("rd_step", C.c_int, [P, i64]),
     ("rd_checkpoint", C.c_int, [P]),

@@ -7,8 +7,21 @@
 
 #include "rd_launch.h"
 
+#include <cstdlib>
+
 namespace rdl {
 namespace detail {
+
+// RD_TB_DSMEM=bytes: dynamic shared memory added to every tb_kernel launch (and
+// to its occupancy query). Measurement only: it caps the resident one-warp
+// CTAs per SM without touching the kernel (occupancy sweep).
+inline size_t tb_dsmem() {
+  static const size_t v = [] {
+    const char* e = std::getenv("RD_TB_DSMEM");
+    return e ? (size_t)std::strtoul(e, nullptr, 10) : (size_t)0;
+  }();
+  return v;
+}
 
 // the default fast mode of each precision (fp32 Table-1: guard-free 4-op
 // division; fp64: FOLD) also has the LEAN / CHECKED tb_kernel variants
@@ -24,15 +37,15 @@ cudaError_t go(const rdk::TBArgs<T>& a, bool lp, int var, unsigned grid, cudaStr
     if (!lp && var == rdk::TB_LEAN) {
       if (occ)
         return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, rdk::tb_kernel<T, K, V, REACT, MODE, rdk::TB_LEAN>,
-                                                             32, 0);
-      rdk::tb_kernel<T, K, V, REACT, MODE, rdk::TB_LEAN><<<grid, 32, 0, st>>>(a);
+                                                             32, tb_dsmem());
+      rdk::tb_kernel<T, K, V, REACT, MODE, rdk::TB_LEAN><<<grid, 32, tb_dsmem(), st>>>(a);
       return cudaGetLastError();
     }
     if (!lp && var == rdk::TB_CHECKED) {
       if (occ)
         return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            occ, rdk::tb_kernel<T, K, V, REACT, MODE, rdk::TB_CHECKED>, 32, 0);
-      rdk::tb_kernel<T, K, V, REACT, MODE, rdk::TB_CHECKED><<<grid, 32, 0, st>>>(a);
+            occ, rdk::tb_kernel<T, K, V, REACT, MODE, rdk::TB_CHECKED>, 32, tb_dsmem());
+      rdk::tb_kernel<T, K, V, REACT, MODE, rdk::TB_CHECKED><<<grid, 32, tb_dsmem(), st>>>(a);
       return cudaGetLastError();
     }
   }
@@ -44,8 +57,8 @@ cudaError_t go(const rdk::TBArgs<T>& a, bool lp, int var, unsigned grid, cudaStr
     }
     return cudaErrorInvalidValue;
   }
-  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, rdk::tb_kernel<T, K, V, REACT, MODE>, 32, 0);
-  rdk::tb_kernel<T, K, V, REACT, MODE><<<grid, 32, 0, st>>>(a);
+  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, rdk::tb_kernel<T, K, V, REACT, MODE>, 32, tb_dsmem());
+  rdk::tb_kernel<T, K, V, REACT, MODE><<<grid, 32, tb_dsmem(), st>>>(a);
   return cudaGetLastError();
 }
 

@@ -146,6 +146,8 @@ struct rd_sim {
   bool defer_samples = false;  // replay: probes / timelapse sampled only after the step's fault check
   bool lean_launch = false;    // the next stencil launch may skip its health check (tb_kernel TB_LEAN)
   int* d_flag = nullptr;
+  int* h_flag = nullptr;      // mapped pinned host word: check_finite_dev's verdict without a copy-engine read
+  int* h_flag_dev = nullptr;  // its device address
   void* d_scratch = nullptr;  // probe max output
   int num_sms = 148;
   // CUDA graphs of rd_step segments, keyed by (length, kmax, start buffer,
@@ -165,6 +167,18 @@ struct rd_sim {
   int64_t acc_timed = 0;
   rd_fault fault{-1, -1, 0, -1, -1};
   std::string err;
+  // asynchronous host I/O (rd_write_fields_async / rd_commit_fields /
+  // rd_read_fields_async / rd_io_wait): dense [plane][b][H][W] staging blocks
+  // and one copy stream per direction, created on first use
+  void* io_in = nullptr;   // inputs uploaded but not yet committed
+  void* io_out = nullptr;  // a snapshot of the fields being copied to the host
+  cudaStream_t io_s_in = nullptr, io_s_out = nullptr;
+  cudaEvent_t io_e_in = nullptr;      // last upload into io_in done
+  cudaEvent_t io_e_commit = nullptr;  // last commit's reads of io_in done
+  cudaEvent_t io_e_snap = nullptr;    // last snapshot into io_out done
+  cudaEvent_t io_e_out = nullptr;     // last download from io_out done
+  std::vector<uint8_t> io_staged;     // [plane * B + b]: uploaded, awaiting rd_commit_fields
+  std::vector<uint8_t> io_draining;   // [plane * B + b]: a download of this slot may be in flight
 };
 
 namespace {
@@ -1174,18 +1188,43 @@ int reset_fault(rd_sim* s) {
   return RD_OK;
 }
 
+// Device-to-device copy of `rows` rows of `row_bytes` bytes on the handle's
+// stream, by copy_rows_kernel (SMs, not a copy engine: see the kernel) when
+// everything is 16-byte aligned, else cudaMemcpy2DAsync.
+int copy_rows(rd_sim* s, void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t row_bytes, int64_t rows) {
+  if (rows <= 0 || row_bytes <= 0) return RD_OK;
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | (uintptr_t)dpitch |
+                        (uintptr_t)spitch | (uintptr_t)row_bytes;
+  if (mis % 16) {
+    RD_CUDA(s, cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyDeviceToDevice, s->stream));
+    return RD_OK;
+  }
+  if (dpitch == row_bytes && spitch == row_bytes) {  // contiguous: one long row
+    row_bytes *= rows;
+    rows = 1;
+  }
+  const int64_t n = row_bytes / 16 * rows;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8 * s->num_sms));
+  rdk::copy_rows_kernel<<<blocks, 256, 0, s->stream>>>(static_cast<char*>(dst), dpitch, static_cast<const char*>(src),
+                                                       spitch, row_bytes, rows);
+  RD_CUDA(s, cudaGetLastError());
+  s->st.launches++;
+  return RD_OK;
+}
+
 // Checkpoint = u, v (current buffers), probe latches, timelapse, step,
 // buffer parity and pending events; restore returns to it exactly.
 int save_checkpoint(rd_sim* s) {
   Range r_("rd_checkpoint");
   if (!s->ck_u) return set_err(s, RD_EINVAL, "handle created with RD_NO_CHECKPOINT");
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
-  RD_CUDA(s, cudaMemcpyAsync(s->ck_u, s->u[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
-  RD_CUDA(s, cudaMemcpyAsync(s->ck_v, s->v[s->cur], bytes, cudaMemcpyDeviceToDevice, s->stream));
+  if (int rc = copy_rows(s, s->ck_u, bytes, s->u[s->cur], bytes, bytes, 1)) return rc;
+  if (int rc = copy_rows(s, s->ck_v, bytes, s->v[s->cur], bytes, bytes, 1)) return rc;
   if (!s->probes.empty())
     RD_CUDA(s, cudaMemcpyAsync(s->d_first_ck, s->d_first, sizeof(long long) * s->probes.size(),
                                cudaMemcpyDeviceToDevice, s->stream));
-  if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->ck_tl, s->tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
+  if (s->tl)
+    if (int rc = copy_rows(s, s->ck_tl, bytes, s->tl, bytes, bytes, 1)) return rc;
   s->ck_step = s->step;
   s->ck_cur = s->cur;
   s->ck_events = s->events;
@@ -1198,12 +1237,13 @@ int restore_checkpoint(rd_sim* s) {
   if (!s->ck_valid) return set_err(s, RD_ERANGE, "no checkpoint to restore");
   const size_t bytes = (size_t)s->B * s->plane_stride * s->esz;
   s->cur = s->ck_cur;
-  RD_CUDA(s, cudaMemcpyAsync(s->u[s->cur], s->ck_u, bytes, cudaMemcpyDeviceToDevice, s->stream));
-  RD_CUDA(s, cudaMemcpyAsync(s->v[s->cur], s->ck_v, bytes, cudaMemcpyDeviceToDevice, s->stream));
+  if (int rc = copy_rows(s, s->u[s->cur], bytes, s->ck_u, bytes, bytes, 1)) return rc;
+  if (int rc = copy_rows(s, s->v[s->cur], bytes, s->ck_v, bytes, bytes, 1)) return rc;
   if (!s->probes.empty())
     RD_CUDA(s, cudaMemcpyAsync(s->d_first, s->d_first_ck, sizeof(long long) * s->probes.size(),
                                cudaMemcpyDeviceToDevice, s->stream));
-  if (s->tl) RD_CUDA(s, cudaMemcpyAsync(s->tl, s->ck_tl, bytes, cudaMemcpyDeviceToDevice, s->stream));
+  if (s->tl)
+    if (int rc = copy_rows(s, s->tl, bytes, s->ck_tl, bytes, bytes, 1)) return rc;
   s->events = s->ck_events;
   s->step = s->ck_step;
   s->ghost_valid = (int32_t)s->halo;
@@ -1247,6 +1287,8 @@ int alloc_planes(rd_sim* s, void* ext, size_t ext_bytes) {
   RD_CUDA(s, cudaMalloc(&s->d_fault, 2 * sizeof(unsigned long long)));
   s->d_precise = reinterpret_cast<int*>(s->d_fault + 1);
   RD_CUDA(s, cudaMalloc(&s->d_flag, sizeof(int)));
+  RD_CUDA(s, cudaHostAlloc(reinterpret_cast<void**>(&s->h_flag), sizeof(int), cudaHostAllocMapped));
+  RD_CUDA(s, cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->h_flag_dev), s->h_flag, 0));
   RD_CUDA(s, cudaMalloc(&s->d_scratch, 64));
   return reset_fault(s);
 }
@@ -1282,20 +1324,25 @@ int encode_tmaps(rd_sim* s) {
   return RD_OK;
 }
 
-int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad) {
-  RD_CUDA(s, cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream));
+int check_finite_dev(rd_sim* s, const void* base, int64_t rows, int* bad, int64_t pitch = 0) {
+  if (pitch == 0) pitch = s->pitch;
+  // The verdict lands in a mapped host word, written by the kernel itself: a
+  // device-to-host memcpy of the flag would queue on the download copy engine
+  // behind an rd_read_fields_async transfer in flight (tens of ms). No kernel
+  // that writes the word is in flight here: every call ends synchronised.
+  *s->h_flag = 0;
   if (rows > 0) {
     const int blocks = 148 * 8;
     if (s->esz == 4)
-      rdk::finite_kernel<float><<<blocks, 256, 0, s->stream>>>((const float*)base, rows, s->W, s->pitch, s->d_flag);
+      rdk::finite_kernel<float><<<blocks, 256, 0, s->stream>>>((const float*)base, rows, s->W, pitch, s->h_flag_dev);
     else
-      rdk::finite_kernel<double><<<blocks, 256, 0, s->stream>>>((const double*)base, rows, s->W, s->pitch,
-                                                                 s->d_flag);
+      rdk::finite_kernel<double><<<blocks, 256, 0, s->stream>>>((const double*)base, rows, s->W, pitch,
+                                                                 s->h_flag_dev);
     RD_CUDA(s, cudaGetLastError());
     s->st.launches++;
   }
-  RD_CUDA(s, cudaMemcpyAsync(bad, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   RD_CUDA(s, cudaStreamSynchronize(s->stream));
+  *bad = *s->h_flag;
   return RD_OK;
 }
 
@@ -1579,6 +1626,132 @@ int write_fields(rd_sim* s, int32_t b, const void* u, const void* v, cudaMemcpyK
                        s->r_hi);
 }
 
+// ---- asynchronous host I/O ---------------------------------------------------
+// Uploads land in a dense staging block on their own copy stream while the
+// handle computes; rd_commit_fields orders the stream behind them, checks them
+// and copies them into the live planes. Downloads snapshot the fields into a
+// second staging block on the compute stream (device-to-device) and drain it
+// to the host on another copy stream, so the next rd_step starts at once.
+int io_init(rd_sim* s) {
+  if (s->io_in) return RD_OK;
+  const size_t bytes = 2 * (size_t)s->B * s->H * s->W * s->esz;
+  RD_CUDA(s, cudaMalloc(&s->io_in, bytes));
+  RD_CUDA(s, cudaMalloc(&s->io_out, bytes));
+  RD_CUDA(s, cudaStreamCreateWithFlags(&s->io_s_in, cudaStreamNonBlocking));
+  RD_CUDA(s, cudaStreamCreateWithFlags(&s->io_s_out, cudaStreamNonBlocking));
+  cudaEvent_t* ev[4] = {&s->io_e_in, &s->io_e_commit, &s->io_e_snap, &s->io_e_out};
+  for (cudaEvent_t* e : ev) RD_CUDA(s, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  s->io_staged.assign(2 * (size_t)s->B, 0);
+  s->io_draining.assign(2 * (size_t)s->B, 0);
+  return RD_OK;
+}
+
+char* io_slot(rd_sim* s, void* block, int plane, int32_t b) {
+  return static_cast<char*>(block) + ((size_t)plane * s->B + b) * (size_t)s->H * s->W * s->esz;
+}
+
+void io_destroy(rd_sim* s) {
+  if (s->io_s_in) cudaStreamSynchronize(s->io_s_in);
+  if (s->io_s_out) cudaStreamSynchronize(s->io_s_out);
+  cudaEvent_t ev[4] = {s->io_e_in, s->io_e_commit, s->io_e_snap, s->io_e_out};
+  for (cudaEvent_t e : ev)
+    if (e) cudaEventDestroy(e);
+  if (s->io_s_in) cudaStreamDestroy(s->io_s_in);
+  if (s->io_s_out) cudaStreamDestroy(s->io_s_out);
+  if (s->io_in) cudaFree(s->io_in);
+  if (s->io_out) cudaFree(s->io_out);
+}
+
+int write_fields_async(rd_sim* s, int32_t b, const void* u, const void* v) {
+  if (int rc = check_b(s, b)) return rc;
+  if (!u && !v) return RD_OK;
+  if (int rc = io_init(s)) return rc;
+  // the last commit may still be reading the staging block
+  RD_CUDA(s, cudaStreamWaitEvent(s->io_s_in, s->io_e_commit, 0));
+  const void* bufs[2] = {u, v};
+  const size_t bytes = (size_t)s->H * s->W * s->esz;
+  for (int k = 0; k < 2; ++k) {
+    if (!bufs[k]) continue;
+    RD_CUDA(s, cudaMemcpyAsync(io_slot(s, s->io_in, k, b), bufs[k], bytes, cudaMemcpyHostToDevice, s->io_s_in));
+    s->io_staged[(size_t)k * s->B + b] = 1;
+  }
+  RD_CUDA(s, cudaEventRecord(s->io_e_in, s->io_s_in));
+  return RD_OK;
+}
+
+int commit_fields(rd_sim* s) {
+  if (!s->io_in) return RD_OK;
+  bool any = false;
+  for (uint8_t f : s->io_staged) any = any || f;
+  if (!any) return RD_OK;
+  Range r_("rd_commit_fields");
+  RD_CUDA(s, cudaStreamWaitEvent(s->stream, s->io_e_in, 0));
+  // all or nothing: every staged plane is checked before any is copied in
+  for (int k = 0; k < 2; ++k)
+    for (int32_t b = 0; b < s->B; ++b) {
+      if (!s->io_staged[(size_t)k * s->B + b]) continue;
+      int bad = 0;
+      if (int rc = check_finite_dev(s, io_slot(s, s->io_in, k, b), s->H, &bad, s->W)) return rc;
+      if (bad) {
+        std::fill(s->io_staged.begin(), s->io_staged.end(), 0);
+        return set_err(s, RD_ENONFINITE, "rd_commit_fields: %s of instance %d contains non-finite values (nothing written)",
+                       k ? "v" : "u", b);
+      }
+    }
+  void* live[2] = {s->u[s->cur], s->v[s->cur]};
+  bool wrote[2] = {false, false};
+  for (int k = 0; k < 2; ++k)
+    for (int32_t b = 0; b < s->B; ++b) {
+      if (!s->io_staged[(size_t)k * s->B + b]) continue;
+      if (int rc = copy_rows(s, plane_ptr(s, live[k], b, 0), s->pitch * s->esz, io_slot(s, s->io_in, k, b),
+                             s->W * s->esz, s->W * s->esz, s->H))
+        return rc;
+      s->io_staged[(size_t)k * s->B + b] = 0;
+      wrote[k] = true;
+    }
+  RD_CUDA(s, cudaEventRecord(s->io_e_commit, s->stream));
+  return launch_mirror(s, wrote[0] ? live[0] : live[1], (wrote[0] && wrote[1]) ? live[1] : nullptr, nullptr, s->r_lo,
+                       s->r_hi);
+}
+
+int read_fields_async(rd_sim* s, int32_t b, void* u_out, void* v_out) {
+  if (int rc = check_b(s, b)) return rc;
+  if (!u_out && !v_out) return RD_OK;
+  if (int rc = io_init(s)) return rc;
+  void* bufs[2] = {u_out, v_out};
+  void* live[2] = {s->u[s->cur], s->v[s->cur]};
+  // a slot still draining an earlier snapshot must finish first
+  if (cudaEventQuery(s->io_e_out) == cudaSuccess) std::fill(s->io_draining.begin(), s->io_draining.end(), 0);
+  for (int k = 0; k < 2; ++k)
+    if (bufs[k] && s->io_draining[(size_t)k * s->B + b]) {
+      RD_CUDA(s, cudaStreamWaitEvent(s->stream, s->io_e_out, 0));
+      break;
+    }
+  for (int k = 0; k < 2; ++k)
+    if (bufs[k])
+      if (int rc = copy_rows(s, io_slot(s, s->io_out, k, b), s->W * s->esz, plane_ptr(s, live[k], b, 0),
+                             s->pitch * s->esz, s->W * s->esz, s->H))
+        return rc;
+  RD_CUDA(s, cudaEventRecord(s->io_e_snap, s->stream));
+  RD_CUDA(s, cudaStreamWaitEvent(s->io_s_out, s->io_e_snap, 0));
+  const size_t bytes = (size_t)s->H * s->W * s->esz;
+  for (int k = 0; k < 2; ++k)
+    if (bufs[k]) {
+      RD_CUDA(s, cudaMemcpyAsync(bufs[k], io_slot(s, s->io_out, k, b), bytes, cudaMemcpyDeviceToHost, s->io_s_out));
+      s->io_draining[(size_t)k * s->B + b] = 1;
+    }
+  RD_CUDA(s, cudaEventRecord(s->io_e_out, s->io_s_out));
+  return RD_OK;
+}
+
+int io_wait(rd_sim* s) {
+  if (!s->io_in) return RD_OK;
+  RD_CUDA(s, cudaStreamSynchronize(s->io_s_in));
+  RD_CUDA(s, cudaStreamSynchronize(s->io_s_out));
+  std::fill(s->io_draining.begin(), s->io_draining.end(), 0);
+  return RD_OK;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -1671,12 +1844,14 @@ int rd_destroy(rd_sim* s) {
   if (!s) return RD_OK;
   if (s->stream) cudaStreamSynchronize(s->stream);
   if (s->dist) dist_destroy(s);
+  io_destroy(s);
   for (void* m : s->ipc_mapped) cudaIpcCloseMemHandle(m);
   if (s->arena && s->own_arena) cudaFree(s->arena);
   void* ps[] = {s->tl,        s->ck_tl,   s->d_probes, s->d_first, s->d_first_ck, s->d_fault,
                 s->d_flag,    s->d_scratch, s->d_idx,  s->d_pal,   s->d_pal_n,    s->gz_x};
   for (void* p : ps)
     if (p) cudaFree(p);
+  if (s->h_flag) cudaFreeHost(s->h_flag);
   for (auto& e : s->ev_pool) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -1717,6 +1892,26 @@ int rd_read_fields_device(rd_sim* s, int32_t b, void* u_out, void* v_out) {
   if (!s) return RD_EINVAL;
   if (int rc = check_b(s, b)) return rc;
   return copy_fields(s, b, u_out, v_out, cudaMemcpyDeviceToDevice, false);
+}
+
+int rd_write_fields_async(rd_sim* s, int32_t b, const void* u, const void* v) {
+  if (!s) return RD_EINVAL;
+  return write_fields_async(s, b, u, v);
+}
+
+int rd_commit_fields(rd_sim* s) {
+  if (!s) return RD_EINVAL;
+  return commit_fields(s);
+}
+
+int rd_read_fields_async(rd_sim* s, int32_t b, void* u_out, void* v_out) {
+  if (!s) return RD_EINVAL;
+  return read_fields_async(s, b, u_out, v_out);
+}
+
+int rd_io_wait(rd_sim* s) {
+  if (!s) return RD_EINVAL;
+  return io_wait(s);
 }
 
 int rd_stimulate(rd_sim* s, int32_t b, const rd_shape* shape, double value, int64_t at_step) {
