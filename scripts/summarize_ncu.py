@@ -57,7 +57,9 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a .csv is the raw page already exported on the GPU box (ncu -i X.ncu-rep --page raw --csv)
+    out = (open(path).read() if path.endswith(".csv") else
+           subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
     rows = list(csv.reader(out.splitlines()))
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = {}
@@ -81,8 +83,10 @@ def main():
     ap.add_argument("--full", default=os.path.join(ROOT, "gpurun_out", "prof_full.ncu-rep"))
     ap.add_argument("--cr", default=os.path.join(ROOT, "gpurun_out", "prof_cr.ncu-rep"),
                     help="--set full capture of cr_kernel (config 2)")
-    ap.add_argument("--gz", default=os.path.join(ROOT, "gpurun_out", "prof_gz.ncu-rep"),
+    ap.add_argument("--gz", default=os.path.join(ROOT, "gpurun_out", "prof_gz_raw.csv"),
                     help="--set full capture of gz_kernel (config 3 fp32)")
+    ap.add_argument("--f64", default=os.path.join(ROOT, "gpurun_out", "prof_tb_f64_raw.csv"),
+                    help="raw page of the --set full capture of tb_kernel<double> on the config-4 grid")
     ap.add_argument("--cmd", default="")
     ap.add_argument("--workload", default="c4_roofline", help="bench workload tag of the --full capture")
     ap.add_argument("--kernel-tag", default="tb_kernel<float,K=4>", help="bench.py's kernel name")
@@ -117,6 +121,12 @@ def main():
         json.dump(F, open(os.path.join(PROF, f"{a.round}_cr_kernel_full.json"), "w"), indent=1)
         print("cr_kernel:", {k: F[k] for k in ("gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in F})
     gz_summary(a)
+    if os.path.exists(a.f64):
+        F = full(a.f64)
+        F["source"] = (f"ncu --set full capture ({os.path.basename(a.f64)}), tb_kernel<double, K=4> (LEAN) on the "
+                       "config-4 grid in fp64 (bench.config4_fp64, scripts/gpu_round2_base.sh)")
+        json.dump(F, open(os.path.join(PROF, f"{a.round}_tb_kernel_f64_full.json"), "w"), indent=1)
+        print("tb_kernel fp64:", {k: F[k] for k in ("gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in F})
 
 
 def gz_summary(a):
