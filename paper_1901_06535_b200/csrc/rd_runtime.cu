@@ -283,19 +283,57 @@ constexpr int vec_of() {
   return 16 / (int)sizeof(T);
 }
 
-// Rows per task. A task costs (hb + 2K) row iterations (the 2K-row pipeline
-// fill/drain is overhead); the persistent CTAs take tasks round-robin, so a
-// launch lasts ~ ceil(tasks / ctas) * (hb + 2K) row iterations, each taking
-// ~max(kLatencyWarps, warps resident per SM) issue-shares of the SM (a lone
-// warp is latency-bound; ~6 warps per SM saturate its issue slots). Pick the
-// hb minimising that: big grids get long tasks and no partial last wave,
-// small batched grids get short tasks spread over the whole chip.
-int pick_hb(const rd_sim* s, int n_strips, int64_t rows, int K, int64_t ctas) {
-  constexpr double kLatencyWarps = 6.0;
+// Rows per task (tb_kernel: one-warp CTAs, `ctas` resident slots). A task
+// runs r = 3 * floor((hb + 2K + 2) / 3) row iterations for hb output rows (the
+// 2K-row pipeline fill/drain is overhead, and the row loop advances three
+// rows per trip); the persistent CTAs take tasks round-robin, so a launch
+// lasts rounds * r row iterations of the slowest warp. A row iteration costs a
+// warp as many issue shares as there are warps on its scheduler (four
+// schedulers per SM), but never fewer than two: measured on B200, two warps
+// per scheduler saturate the issue slots (8 CTAs per SM run config 4 as fast
+// as 16) and a lone warp runs no faster than one of two (grids of 2048^2 to
+// 4096^2: 5 warps per SM reach 0.73 of the rate of 8, 10 reach 0.92, 8 and 16
+// are level). Launches with enough work (at 64 rows per task they would fill
+// 0.9 of the slots) take the hb minimising rounds * r * shares: long tasks on
+// every slot, or exactly two warps per scheduler, instead of a ragged count.
+// Smaller launches keep the round-1 latency model below, which measured
+// better there (B200, fp32 / fp64 Gcell/s, this model vs round 1: 2048^2
+// 352 / 252 vs 408 / 287; 4096^2 700 / 342 vs 653 / 287; 6144^2 985 vs 780;
+// 8192^2 1017 vs 944; config 4: the same hb either way).
+// (RD_HB=n fixes hb; RD_HB_MODEL=r01 | r02 forces one model.)
+int pick_hb(const rd_sim* s, int n_strips, int64_t rows, int K, int64_t ctas, bool one_warp_ctas) {
   if (const char* e = getenv("RD_HB")) {
     int hb = atoi(e);
     if (hb >= 1) return hb;
   }
+  static const int force_model = [] {
+    const char* e = getenv("RD_HB_MODEL");
+    return !e ? 0 : (std::string(e) == "r01" ? 1 : (std::string(e) == "r02" ? 2 : 0));
+  }();
+  const bool big = 10 * (int64_t)n_strips * s->B * ((rows + 63) / 64) >= 9 * ctas;
+  if (one_warp_ctas && force_model != 1 && (big || force_model == 2)) {
+    int best = 1;
+    double best_cost = 1e300;
+    const int64_t hb_max = std::min<int64_t>(rows, 2048);
+    for (int64_t hb = 1; hb <= hb_max; ++hb) {
+      const int64_t tasks = (int64_t)n_strips * ((rows + hb - 1) / hb) * s->B;
+      const int64_t grid = std::min<int64_t>(tasks, ctas);
+      const int64_t rounds = (tasks + grid - 1) / grid;
+      const int64_t per_sm = (grid + s->num_sms - 1) / s->num_sms;  // resident warps on the fullest SM
+      const int64_t shares = std::max<int64_t>(2, (per_sm + 3) / 4);
+      const int64_t r = 3 * ((hb + 2 * K + 2) / 3);
+      // ties: the taller block (less fill/drain traffic)
+      const double cost = (double)(rounds * r * shares) - 1e-6 * (double)hb;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = (int)hb;
+      }
+    }
+    return best;
+  }
+  // lp_kernel (CTAs of K warps) and the round-1 model: a task costs (hb + 2K)
+  // row iterations, each ~max(kLatencyWarps, warps resident per SM) issue shares
+  constexpr double kLatencyWarps = 6.0;
   int best = 1;
   double best_cost = 1e300;
   for (int hb = 1; hb <= 1024; ++hb) {
@@ -310,10 +348,8 @@ int pick_hb(const rd_sim* s, int n_strips, int64_t rows, int K, int64_t ctas) {
     if (hb >= rows) break;
   }
   // Large grids (the chosen split is one wave filling at least half of the
-  // resident slots): per-SM throughput keeps rising up to the full 16 CTAs
-  // (config 4: 2329 tasks of 964 rows beat 2192 of 1024 by 8% per clock), so
-  // use the smallest row block that still fits one wave -- every slot busy,
-  // no second wave.
+  // resident slots): use the smallest row block that still fits one wave --
+  // every slot busy, no second wave.
   const int64_t tasks_best = (int64_t)n_strips * ((rows + best - 1) / best) * s->B;
   if (tasks_best <= ctas && 2 * tasks_best >= ctas) {
     const int64_t per_strip = ctas / ((int64_t)n_strips * s->B);  // row blocks per (strip, instance)
@@ -432,7 +468,7 @@ cudaError_t launch_stencil(rd_sim* s, int k, int in, int out, int32_t out_lo, in
     var = s->lean_launch ? rdk::TB_LEAN : rdk::TB_CHECKED;
   const int64_t ctas = (int64_t)s->num_sms * rdl::occupancy_tb(sizeof(T) == 4, k, mode, react, lp, var);
   // lp: a task costs ~hb + 3K rows
-  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, lp ? k + (k + 1) / 2 : k, ctas);
+  a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, lp ? k + (k + 1) / 2 : k, ctas, !lp);
   const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
   return rdl::launch_tb(a, k, mode, react, lp, var, (unsigned)std::min<int64_t>(tasks, ctas), s->stream);
 }

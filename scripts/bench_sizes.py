@@ -1,0 +1,68 @@
+#!/usr/bin/env python
+"""Throughput against grid size (informational): one instance of side n (or a
+batch), uniform phi, seeded noise, a few stimuli, `--steps` time steps through
+rd_step with the default kernel choice. Shows where gz_kernel hands over to
+tb_kernel and what the sizes in between reach. One JSON line per size.
+
+  python scripts/bench_sizes.py [--sizes 128,256,8192x65536,...] [--dtype f32|f64] [--kernel auto|tb|gz|cr]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1901_06535_b200 as rd  # noqa: E402
+
+
+def run(n, dtype, steps, batch):
+    h, w = (int(x) for x in n.split("x")) if "x" in n else (int(n), int(n))
+    n = h
+    sim = rd.Sim(None, shape=(batch, h, w), dtype=dtype)
+    sim.paint_phi(0.054)
+    sim.fill_noise(seed=1)
+    sim.stimulate({"kind": "disc", "cy2": h, "cx2": w, "r": 6}, 1.0, 0)
+    stream = torch.cuda.current_stream()
+    sim.set_stream(stream)
+    ms = None
+    for _ in range(2):  # the second run is reported (graphs captured, clocks up)
+        rd.rd_reset_stats(sim.h)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        sim.step(steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    st = sim.stats()
+    sim.close()
+    return {"side": n, "width": w, "batch": batch, "dtype": np.dtype(dtype).name, "steps": steps, "device_ms": ms,
+            "us_per_step": ms * 1e3 / steps, "gcell_updates_per_s": batch * h * w * steps / (ms / 1e3) / 1e9,
+            "stencil_kernel": ["tb", "lp", "cr", "gz"][st["kernel"]], "tb_depth": st["tb_depth"],
+            "launches": st["launches"]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="128,256,384,512,768,1024,1536,2048,3072,4096,8192")
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--kernel", default="auto")
+    a = ap.parse_args()
+    os.environ["RD_KERNEL"] = a.kernel
+    dt = np.float32 if a.dtype == "f32" else np.float64
+    for n in a.sizes.split(","):
+        cells = int(n.split("x")[0]) * int(n.split("x")[-1])
+        steps = a.steps if cells <= 4096 * 4096 else max(200, a.steps // 4)
+        print(json.dumps(run(n, dt, steps, a.batch)), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,6 +1,7 @@
 /* The C ABI used from plain C (no Python): create a two-instance batch,
  * schedule stimuli, step in two calls, read fields, probe -- and compare with
- * the oracle's C library bitwise, in fp64 and fp32. Also checks error codes.
+ * the oracle's C library bitwise, in fp64 and fp32; then the asynchronous
+ * host I/O calls (stage, snapshot, commit, step). Also checks error codes.
  * Test program only: it links the oracle (tests/ may), the product does not.
  *   gcc -O2 -Iinclude -Ioracle tests/c/abi_c_demo.c -Lpaper_1901_06535_b200 -lrd -Loracle -lorc */
 #include <math.h>
@@ -96,6 +97,41 @@ static int run(int dtype) {
       fprintf(stderr, "probe %d: %g vs %g\n", b, mx, omx);
       bad = 1;
     }
+  }
+  /* asynchronous host I/O: stage the oracle's last fields (instance B-1's,
+   * still in ru / rv) as new inputs of instance 0, snapshot instance 0 before
+   * the commit, commit, step, and compare with the oracle continuing from
+   * those inputs on instance 0's phi */
+  {
+    unsigned char* su = calloc(n, esz);
+    unsigned char* sv = calloc(n, esz);
+    enum { MORE = 7 };
+    int rc2 = rd_write_fields_async(s, 0, ru, rv);
+    rc2 |= rd_read_fields_async(s, 0, su, sv);
+    rc2 |= rd_commit_fields(s);
+    rc2 |= rd_step(s, MORE);
+    rc2 |= rd_io_wait(s);
+    if (rc2 != RD_OK || rd_write_fields_async(s, B, ru, rv) != RD_ERANGE) {
+      fprintf(stderr, "async I/O: %s\n", rd_last_error(s));
+      return 1;
+    }
+    if (memcmp(su, u, n * esz) || memcmp(sv, v, n * esz)) {
+      fprintf(stderr, "async snapshot differs from the fields before the commit\n");
+      bad = 1;
+    }
+    if (rd_read_fields(s, 0, su, sv) != RD_OK) return 1;
+    orc_params op;
+    orc_params_default(&op);
+    orc_fault f;
+    const int st = esz == 8 ? orc_run_f64(H, W, (double*)ru, (double*)rv, (double*)phi, &op, 0, 0, MORE, NULL, 0, NULL, 0,
+                                          NULL, &f, 0, NULL)
+                            : orc_run_f32(H, W, (float*)ru, (float*)rv, (float*)phi, &op, 0, 0, MORE, NULL, 0, NULL, 0,
+                                          NULL, &f, 0, NULL);
+    if (st != 0 || memcmp(su, ru, n * esz) || memcmp(sv, rv, n * esz)) {
+      fprintf(stderr, "async commit + steps differ from the oracle (%s)\n", esz == 8 ? "f64" : "f32");
+      bad = 1;
+    }
+    free(su), free(sv);
   }
   rd_destroy(s);
   free(phi), free(u), free(v), free(ru), free(rv);
