@@ -291,7 +291,8 @@ def roofline_of(st, ms, workload_tag, dtype):
     achieved = bpc * st["cell_updates"] / (kms / 1e3) / 1e9 if kms > 0 else None
     alu, alu_src = alu_peak_tops()
     ops = OPS_PER_CELL * st["cell_updates"] / (kms / 1e3) / 1e12 if kms > 0 else None
-    kernel = f"tb_kernel<float,K={st['tb_depth']}>"
+    # the handle found phi to be one value: tb_kernel takes it as a parameter (its UPHI variants)
+    kernel = f"tb_kernel<float,K={st['tb_depth']}{',uphi' if st.get('phi_uniform') else ''}>"
     cpl = st["cell_updates"] / k_launches
     traffic, tsrc = load_traffic(workload_tag, kernel, cpl)
     return {"bound": "alu", "achieved": ops, "peak": alu, "unit": "TFLOP/s",
@@ -304,7 +305,10 @@ def roofline_of(st, ms, workload_tag, dtype):
             "kernel_share_of_step": kms / ms if ms else None,
             "hbm_view": {"achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "peak_source": hbm_src,
-                         "algorithmic_bytes_per_cell_update": bpc, "one_step_roofline_gcells": hbm / bpc}}
+                         "algorithmic_bytes_per_cell_update": bpc, "one_step_roofline_gcells": hbm / bpc,
+                         "note": ("SURVEY 8(d)'s 20 B per cell-update (read u, v, phi; write u, v); this workload's "
+                                  "phi is one value, which the kernel takes as a parameter (16 B)"
+                                  if st.get("phi_uniform") else None)}}
 
 
 def timed(ctx, stepper, h, T, steps, warmup, clocks_index):
@@ -523,6 +527,24 @@ def run_single(args):
             e2e = e2e_pipelined(rd, sim, pu, pv, T, args.e2e_pipeline_steps, cells)
             e2e["serial"] = {"value": serial["value"], "steps": serial["steps"], "api": serial["api"]}
     launches = st["launches"]
+    # config 4's phi is one value, which tb_kernel takes as a kernel parameter
+    # (rd_stats.phi_uniform); beside the line's value goes the rate of the
+    # general kernel that streams the phi plane (maps with more than one
+    # value: config 5, the circuits), on the same handle: RD_TB_UPHI=0 and a
+    # repaint make the handle re-derive its choice
+    streamed = None
+    if st.get("phi_uniform"):
+        rd.rd_set_stream(h, rd.stream_handle(stream))
+        os.environ["RD_TB_UPHI"] = "0"
+        try:
+            sim.paint_phi(0.054)
+            sms, sst, sclk = timed(ctx, sim.step, h, T, max(2, args.steps // 3), 1, 0)
+            streamed = {"value": cells * T * max(2, args.steps // 3) / (sms / 1e3) / 1e9, "unit": UNIT,
+                        "phi_uniform": sst.get("phi_uniform"), "sm_mhz": (sclk or {}).get("sm_mhz"),
+                        "avg_launch_ms": sst["step_kernel_ms"] / max(1, sst["timed_launches"]),
+                        "what": "the same workload with tb_kernel streaming the phi plane (RD_TB_UPHI=0)"}
+        finally:
+            os.environ.pop("RD_TB_UPHI", None)
     sim.close()
     cpu = None if args.no_cpu_baseline else cpu_baseline(u0, v0, phi, args.cpu_seconds)
     hbm, _ = peaks()
@@ -531,7 +553,8 @@ def run_single(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_dict(1, T, st["tb_depth"]),
             "frac_of_one_step_hbm_roofline": value / (hbm / BYTES_PER_CELL[dtype]),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "phi_uniform": bool(st.get("phi_uniform")), "phi_streamed": streamed}
     if not args.no_configs:
         line["per_config"] = per_config(0 if args.no_cpu_baseline else args.config_cpu_seconds)
         line["fp32_error"] = fp32_error()

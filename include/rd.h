@@ -131,12 +131,15 @@ typedef struct {
   double step_kernel_ms;   /* summed CUDA-event durations of stencil launches (profiling on) */
   int64_t timed_launches;  /* stencil launches covered by step_kernel_ms */
   int32_t tb_depth;        /* temporal-blocking depth in use */
-  int32_t pad;
+  int32_t phi_uniform;     /* 1: the phi map is one value over every instance (checked on the device after
+                              each change of phi), so tb_kernel takes it as a kernel parameter instead of
+                              streaming the plane (plain single-GPU handles; results are identical) */
   int64_t replays;         /* rd_step calls replayed from the checkpoint (fault or fast-division guard) */
   int32_t arith_mode;      /* 0 precise (canonical ops), 2 exact rewrites, 3 exact rewrites + certified 4-op fp32 division,
                               4 as 3 without the min|C+q| guard (fp32 q >= 2^-35) */
   int32_t kernel;          /* stencil kernel of the fast path: 0 tb_kernel (temporal-blocked streaming),
-                              1 lp_kernel (level-parallel), 2 cr_kernel (cluster-resident, a8) */
+                              1 lp_kernel (level-parallel), 2 cr_kernel (cluster-resident, a8),
+                              3 gz_kernel (whole-chip tiles, a8) */
 } rd_stats;
 
 /* Where a handle's rows sit (rd_get_geometry). For rd_create / rd_create_device
@@ -186,7 +189,9 @@ int rd_destroy(struct rd_sim* sim);
  *                     [batch][height][width] of dtype (or NULL = 0).
  *   rd_field_ptr      instance b's current u (plane 0), v (1) or phi (2):
  *                     device pointer of cell (0, 0), row pitch in elements.
- *                     Valid until the next rd_step (u, v ping-pong).
+ *                     Valid until the next rd_step (u, v ping-pong). Once phi's
+ *                     pointer has been handed out the handle assumes nothing
+ *                     about phi's values (rd_stats.phi_uniform stays 0).
  * Errors: RD_EINVAL (NULL / misaligned / too small arena, bad plane),
  * RD_ERANGE (b), plus those of rd_create. */
 int rd_arena_bytes(const rd_grid* grid, size_t* bytes);

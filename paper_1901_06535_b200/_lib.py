@@ -50,7 +50,7 @@ class rd_fault(C.Structure):
 class rd_stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("step_launches", C.c_int64), ("cell_updates", C.c_int64),
                 ("step_kernel_ms", C.c_double), ("timed_launches", C.c_int64), ("tb_depth", C.c_int32),
-                ("pad", C.c_int32), ("replays", C.c_int64), ("arith_mode", C.c_int32), ("kernel", C.c_int32)]
+                ("phi_uniform", C.c_int32), ("replays", C.c_int64), ("arith_mode", C.c_int32), ("kernel", C.c_int32)]
 
 
 class rd_geometry(C.Structure):

@@ -15,15 +15,21 @@ namespace rdl {
 // tb_kernel (one-warp CTAs). An unsupported combination returns
 // cudaErrorInvalidValue.
 // var: rdk::TB_FULL / TB_LEAN / TB_CHECKED (tb_kernel variants).
-int occupancy_tb_f32(int K, int mode, bool react, bool lp, int var);  // resident CTAs per SM (>= 1)
-int occupancy_tb_f64(int K, int mode, bool react, bool lp, int var);
-inline int occupancy_tb(bool f32, int K, int mode, bool react, bool lp, int var) {
-  return f32 ? occupancy_tb_f32(K, mode, react, lp, var) : occupancy_tb_f64(K, mode, react, lp, var);
+// uphi: the uniform-phi tb_kernel (TBArgs::phi_u), only where tb_uphi_ok.
+int occupancy_tb_f32(int K, int mode, bool react, bool lp, int var, bool uphi);  // resident CTAs per SM (>= 1)
+int occupancy_tb_f64(int K, int mode, bool react, bool lp, int var, bool uphi);
+inline int occupancy_tb(bool f32, int K, int mode, bool react, bool lp, int var, bool uphi) {
+  return f32 ? occupancy_tb_f32(K, mode, react, lp, var, uphi) : occupancy_tb_f64(K, mode, react, lp, var, uphi);
 }
-cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, int var, unsigned grid,
-                      cudaStream_t st);
-cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react, bool lp, int var, unsigned grid,
-                      cudaStream_t st);
+cudaError_t launch_tb(const rdk::TBArgs<float>& a, int K, int mode, bool react, bool lp, int var, bool uphi,
+                      unsigned grid, cudaStream_t st);
+cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react, bool lp, int var, bool uphi,
+                      unsigned grid, cudaStream_t st);
+// the uniform-phi tb_kernel is instantiated for K <= 4, reaction on, in the
+// default fast mode of the precision (fp32: guard-free 4-op division; fp64: FOLD)
+inline bool tb_uphi_ok(bool f32, int K, int mode, bool react, bool lp) {
+  return K <= 4 && react && !lp && mode == (f32 ? rdk::MODE_FOLD_DIV4_NG : rdk::MODE_FOLD);
+}
 
 // cr_kernel over `batch` clusters of cs CTAs with `smem` dynamic shared memory
 // (pal: phi as palette indices). query: return the co-resident cluster count

@@ -30,9 +30,32 @@ constexpr bool has_variants() {
   return sizeof(T) == 4 ? MODE == rdk::MODE_FOLD_DIV4_NG : MODE == rdk::MODE_FOLD;
 }
 
-template <typename T, int K, bool REACT, int MODE>
-cudaError_t go(const rdk::TBArgs<T>& a, bool lp, int var, unsigned grid, cudaStream_t st, int* occ) {
+template <typename T, int K, bool REACT, int MODE, int VAR>
+cudaError_t go_uphi(const rdk::TBArgs<T>& a, unsigned grid, cudaStream_t st, int* occ) {
   constexpr int V = 16 / (int)sizeof(T);
+  if (occ)
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, rdk::tb_kernel<T, K, V, REACT, MODE, VAR, true>, 32,
+                                                         tb_dsmem());
+  rdk::tb_kernel<T, K, V, REACT, MODE, VAR, true><<<grid, 32, tb_dsmem(), st>>>(a);
+  return cudaGetLastError();
+}
+
+// uphi: the uniform-phi tb_kernel (TBArgs::phi_u), instantiated for K <= 4 in
+// the default fast mode of each precision (rdl::tb_uphi_ok).
+template <typename T, int K, bool REACT, int MODE>
+cudaError_t go(const rdk::TBArgs<T>& a, bool lp, int var, bool uphi, unsigned grid, cudaStream_t st, int* occ) {
+  constexpr int V = 16 / (int)sizeof(T);
+  if (uphi) {
+    if constexpr (K <= 4 && REACT && has_variants<T, MODE>()) {
+      if (lp) return cudaErrorInvalidValue;
+      switch (var) {
+        case rdk::TB_LEAN: return go_uphi<T, K, REACT, MODE, rdk::TB_LEAN>(a, grid, st, occ);
+        case rdk::TB_CHECKED: return go_uphi<T, K, REACT, MODE, rdk::TB_CHECKED>(a, grid, st, occ);
+        default: return go_uphi<T, K, REACT, MODE, rdk::TB_FULL>(a, grid, st, occ);
+      }
+    }
+    return cudaErrorInvalidValue;
+  }
   if constexpr (REACT && has_variants<T, MODE>()) {
     if (!lp && var == rdk::TB_LEAN) {
       if (occ)
@@ -63,16 +86,17 @@ cudaError_t go(const rdk::TBArgs<T>& a, bool lp, int var, unsigned grid, cudaStr
 }
 
 template <typename T, bool REACT, int MODE>
-cudaError_t by_k(const rdk::TBArgs<T>& a, int K, bool lp, int var, unsigned grid, cudaStream_t st, int* occ) {
+cudaError_t by_k(const rdk::TBArgs<T>& a, int K, bool lp, int var, bool uphi, unsigned grid, cudaStream_t st,
+                 int* occ) {
   switch (K) {
-    case 1: return go<T, 1, REACT, MODE>(a, lp, var, grid, st, occ);
-    case 2: return go<T, 2, REACT, MODE>(a, lp, var, grid, st, occ);
-    case 3: return go<T, 3, REACT, MODE>(a, lp, var, grid, st, occ);
-    case 4: return go<T, 4, REACT, MODE>(a, lp, var, grid, st, occ);
-    case 5: return go<T, 5, REACT, MODE>(a, lp, var, grid, st, occ);
-    case 6: return go<T, 6, REACT, MODE>(a, lp, var, grid, st, occ);
-    case 7: return go<T, 7, REACT, MODE>(a, lp, var, grid, st, occ);
-    case 8: return go<T, 8, REACT, MODE>(a, lp, var, grid, st, occ);
+    case 1: return go<T, 1, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
+    case 2: return go<T, 2, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
+    case 3: return go<T, 3, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
+    case 4: return go<T, 4, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
+    case 5: return go<T, 5, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
+    case 6: return go<T, 6, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
+    case 7: return go<T, 7, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
+    case 8: return go<T, 8, REACT, MODE>(a, lp, var, uphi, grid, st, occ);
   }
   return cudaErrorInvalidValue;
 }
@@ -81,33 +105,33 @@ cudaError_t by_k(const rdk::TBArgs<T>& a, int K, bool lp, int var, unsigned grid
 // var: rdk::TB_FULL / TB_LEAN / TB_CHECKED (the variants exist for the
 // default fast mode only; any other combination runs TB_FULL)
 template <typename T>
-cudaError_t dispatch(const rdk::TBArgs<T>& a, int K, int mode, bool react, bool lp, int var, unsigned grid,
-                     cudaStream_t st, int* occ) {
-  if (!react) return by_k<T, false, rdk::MODE_PRECISE>(a, K, lp, var, grid, st, occ);
+cudaError_t dispatch(const rdk::TBArgs<T>& a, int K, int mode, bool react, bool lp, int var, bool uphi,
+                     unsigned grid, cudaStream_t st, int* occ) {
+  if (!react) return by_k<T, false, rdk::MODE_PRECISE>(a, K, lp, var, uphi, grid, st, occ);
   switch (mode) {
-    case rdk::MODE_PRECISE: return by_k<T, true, rdk::MODE_PRECISE>(a, K, lp, var, grid, st, occ);
-    case rdk::MODE_FOLD: return by_k<T, true, rdk::MODE_FOLD>(a, K, lp, var, grid, st, occ);
+    case rdk::MODE_PRECISE: return by_k<T, true, rdk::MODE_PRECISE>(a, K, lp, var, uphi, grid, st, occ);
+    case rdk::MODE_FOLD: return by_k<T, true, rdk::MODE_FOLD>(a, K, lp, var, uphi, grid, st, occ);
   }
   if constexpr (sizeof(T) == 4) {
     switch (mode) {
-      case rdk::MODE_FOLD_DIV4: return by_k<T, true, rdk::MODE_FOLD_DIV4>(a, K, lp, var, grid, st, occ);
-      case rdk::MODE_FOLD_DIV4_NG: return by_k<T, true, rdk::MODE_FOLD_DIV4_NG>(a, K, lp, var, grid, st, occ);
+      case rdk::MODE_FOLD_DIV4: return by_k<T, true, rdk::MODE_FOLD_DIV4>(a, K, lp, var, uphi, grid, st, occ);
+      case rdk::MODE_FOLD_DIV4_NG: return by_k<T, true, rdk::MODE_FOLD_DIV4_NG>(a, K, lp, var, uphi, grid, st, occ);
     }
   }
   return cudaErrorInvalidValue;
 }
 
 template <typename T>
-int occupancy(int K, int mode, bool react, bool lp, int var) {
+int occupancy(int K, int mode, bool react, bool lp, int var, bool uphi) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, bool, bool, int>, int> cache;
+  static std::map<std::tuple<int, int, bool, bool, int, bool>, int> cache;
   std::lock_guard<std::mutex> g(mu);
-  const auto key = std::make_tuple(K, mode, react, lp, var);
+  const auto key = std::make_tuple(K, mode, react, lp, var, uphi);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int occ = 0;
   rdk::TBArgs<T> dummy;
-  if (dispatch<T>(dummy, K, mode, react, lp, var, 0, nullptr, &occ) != cudaSuccess || occ < 1) occ = 1;
+  if (dispatch<T>(dummy, K, mode, react, lp, var, uphi, 0, nullptr, &occ) != cudaSuccess || occ < 1) occ = 1;
   cache[key] = occ;
   return occ;
 }

@@ -146,8 +146,13 @@ struct rd_sim {
   bool defer_samples = false;  // replay: probes / timelapse sampled only after the step's fault check
   bool lean_launch = false;    // the next stencil launch may skip its health check (tb_kernel TB_LEAN)
   int* d_flag = nullptr;
-  int* h_flag = nullptr;      // mapped pinned host word: check_finite_dev's verdict without a copy-engine read
-  int* h_flag_dev = nullptr;  // its device address
+  int* h_flag = nullptr;      // mapped pinned host words: check_finite_dev's / phi_uniform_kernel's verdict
+  int* h_flag_dev = nullptr;  // (without a copy-engine read); [0] flag, bytes 8..15 a value. Device address.
+  // whether the phi map is one value (tb_kernel UPHI variants): re-derived on
+  // the device at the next run_range after anything wrote phi
+  bool phi_class_known = false, phi_uniform = false;
+  bool phi_external = false;  // rd_field_ptr handed out phi: the caller may write it at any time
+  double phi_u = 0.0;
   void* d_scratch = nullptr;  // probe max output
   int num_sms = 148;
   // CUDA graphs of rd_step segments, keyed by (length, kmax, start buffer,
@@ -466,11 +471,13 @@ cudaError_t launch_stencil(rd_sim* s, int k, int in, int out, int32_t out_lo, in
   int var = rdk::TB_FULL;
   if (mode != rdk::MODE_PRECISE && !a.tl && !s->push_active && !force_full)
     var = s->lean_launch ? rdk::TB_LEAN : rdk::TB_CHECKED;
-  const int64_t ctas = (int64_t)s->num_sms * rdl::occupancy_tb(sizeof(T) == 4, k, mode, react, lp, var);
+  const bool uphi = s->phi_class_known && s->phi_uniform && rdl::tb_uphi_ok(sizeof(T) == 4, k, mode, react, lp);
+  a.phi_u = (T)s->phi_u;
+  const int64_t ctas = (int64_t)s->num_sms * rdl::occupancy_tb(sizeof(T) == 4, k, mode, react, lp, var, uphi);
   // lp: a task costs ~hb + 3K rows
   a.hb = pick_hb(s, a.n_strips, out_hi - out_lo, lp ? k + (k + 1) / 2 : k, ctas, !lp);
   const int64_t tasks = (int64_t)a.n_strips * ((out_hi - out_lo + a.hb - 1) / a.hb) * s->B;
-  return rdl::launch_tb(a, k, mode, react, lp, var, (unsigned)std::min<int64_t>(tasks, ctas), s->stream);
+  return rdl::launch_tb(a, k, mode, react, lp, var, uphi, (unsigned)std::min<int64_t>(tasks, ctas), s->stream);
 }
 
 // One stencil launch of k steps from buffer `in` to `out` producing rows
@@ -1157,9 +1164,54 @@ void drop_graphs(rd_sim* s) {
 }
 
 // Advance from s->step to end with blocks of at most kmax steps.
+// Whether phi is one value over all instances (then tb_kernel reads it as a
+// kernel parameter): one pass over the map on the device after
+// anything wrote it (create, rd_paint_phi), the verdict and the value in
+// mapped host words. Slab and dist handles recompute ghost rows whose phi
+// comes from the neighbours, so they keep the general kernel. A change of
+// class drops the captured graphs (they bake the kernel variant).
+// RD_TB_UPHI=0 keeps the general kernel (tests run both).
+void drop_graphs(rd_sim* s);
+int ensure_phi_class(rd_sim* s) {
+  if (s->phi_class_known) return RD_OK;
+  bool uni = false;
+  double val = 0.0;
+  const char* e = getenv("RD_TB_UPHI");
+  if (!(e && atoi(e) == 0) && !s->slab && !s->dist && !s->phi_external) {
+    RD_CUDA(s, cudaStreamSynchronize(s->stream));
+    *s->h_flag = 0;
+    const unsigned blocks = (unsigned)(8 * s->num_sms);
+    if (s->esz == 4)
+      rdk::phi_uniform_kernel<float><<<blocks, 256, 0, s->stream>>>(origin<float>(s, s->phi), s->plane_stride, s->pitch,
+                                                                    (int32_t)s->H, (int32_t)s->W, (int32_t)s->B,
+                                                                    s->h_flag_dev, s->h_flag_dev + 2);
+    else
+      rdk::phi_uniform_kernel<double><<<blocks, 256, 0, s->stream>>>(origin<double>(s, s->phi), s->plane_stride,
+                                                                     s->pitch, (int32_t)s->H, (int32_t)s->W,
+                                                                     (int32_t)s->B, s->h_flag_dev, s->h_flag_dev + 2);
+    RD_CUDA(s, cudaGetLastError());
+    s->st.launches++;
+    RD_CUDA(s, cudaStreamSynchronize(s->stream));
+    uni = *s->h_flag == 0;
+    if (s->esz == 4) {
+      float f;
+      std::memcpy(&f, s->h_flag + 2, 4);
+      val = f;
+    } else {
+      std::memcpy(&val, s->h_flag + 2, 8);
+    }
+  }
+  if (uni != s->phi_uniform) drop_graphs(s);
+  s->phi_uniform = uni;
+  s->phi_u = val;
+  s->phi_class_known = true;
+  return RD_OK;
+}
+
 int run_range(rd_sim* s, int64_t end, int kmax) {
-  int rc = sync_probes(s);
+  int rc = ensure_phi_class(s);
   if (rc) return rc;
+  if ((rc = sync_probes(s))) return rc;
   while (s->step < end) {
     // a1: stimuli due now, in submission order; then refresh u's mirrors
     bool stamped = false;
@@ -1323,7 +1375,7 @@ int alloc_planes(rd_sim* s, void* ext, size_t ext_bytes) {
   RD_CUDA(s, cudaMalloc(&s->d_fault, 2 * sizeof(unsigned long long)));
   s->d_precise = reinterpret_cast<int*>(s->d_fault + 1);
   RD_CUDA(s, cudaMalloc(&s->d_flag, sizeof(int)));
-  RD_CUDA(s, cudaHostAlloc(reinterpret_cast<void**>(&s->h_flag), sizeof(int), cudaHostAllocMapped));
+  RD_CUDA(s, cudaHostAlloc(reinterpret_cast<void**>(&s->h_flag), 16, cudaHostAllocMapped));
   RD_CUDA(s, cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->h_flag_dev), s->h_flag, 0));
   RD_CUDA(s, cudaMalloc(&s->d_scratch, 64));
   return reset_fault(s);
@@ -1851,6 +1903,12 @@ int rd_field_ptr(rd_sim* s, int32_t b, int32_t plane, void** ptr, int64_t* pitch
   if (plane < 0 || plane > 2) return set_err(s, RD_EINVAL, "plane must be 0 (u), 1 (v) or 2 (phi)");
   if (s->margins_stale && plane < 2)
     if (int rc = fresh_margins(s)) return rc;
+  if (plane == 2) {
+    // the caller may write phi through this pointer at any later time: never
+    // again assume it is one value (tb_kernel UPHI variants)
+    s->phi_external = true;
+    s->phi_class_known = false;
+  }
   *ptr = plane_ptr(s, planes[plane], b, 0);
   if (pitch_elems) *pitch_elems = s->pitch;
   return RD_OK;
@@ -2381,6 +2439,7 @@ int rd_paint_phi(rd_sim* s, int32_t b, const rd_rect* r, double value) {
       s->st.launches++;
     }
   }
+  s->phi_class_known = false;  // re-derived at the next run_range (ensure_phi_class)
   return launch_mirror(s, s->phi, nullptr, nullptr, s->r_lo, s->r_hi);
 }
 
@@ -2499,6 +2558,7 @@ int rd_get_stats(rd_sim* s, rd_stats* out) {
   out->step_kernel_ms = s->acc_ms;
   out->timed_launches = s->acc_timed;
   out->tb_depth = s->K;
+  out->phi_uniform = (s->phi_class_known && s->phi_uniform) ? 1 : 0;
   out->arith_mode = (s->g.flags & RD_NO_CHECKPOINT) ? rdk::MODE_PRECISE : s->fast_mode;
   out->kernel = (s->use_gz && !(s->g.flags & RD_NO_CHECKPOINT))
                     ? 3

@@ -22,12 +22,18 @@ def table1():
     return golden("table1_params.json")
 
 
-@pytest.fixture(params=["tb", "lp", "cr", "gz"])
+@pytest.fixture(params=["tb", "tb-phimap", "lp", "cr", "gz"])
 def kernel(request, monkeypatch):
     """Run a GPU test with each stencil kernel: the register-pipelined
     tb_kernel, the level-parallel lp_kernel, the cluster-resident cr_kernel
     and the whole-chip tiled gz_kernel (RD_KERNEL, read at rd_create; cr / gz
     apply where the instance fits their limits, else the handle falls back to
-    tb_kernel)."""
-    monkeypatch.setenv("RD_KERNEL", request.param)
-    return request.param
+    tb_kernel). "tb" lets tb_kernel take a one-valued phi map as a kernel
+    parameter (its UPHI variants); "tb-phimap" makes it stream the phi plane
+    whatever its values (RD_TB_UPHI=0), so both paths see every case."""
+    name = request.param
+    if name == "tb-phimap":
+        monkeypatch.setenv("RD_TB_UPHI", "0")
+        name = "tb"
+    monkeypatch.setenv("RD_KERNEL", name)
+    return name
