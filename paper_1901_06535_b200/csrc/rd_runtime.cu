@@ -296,27 +296,24 @@ constexpr int vec_of() {
 // warp as many issue shares as there are warps on its scheduler (four
 // schedulers per SM), but never fewer than two: measured on B200, two warps
 // per scheduler saturate the issue slots (8 CTAs per SM run config 4 as fast
-// as 16) and a lone warp runs no faster than one of two (grids of 2048^2 to
-// 4096^2: 5 warps per SM reach 0.73 of the rate of 8, 10 reach 0.92, 8 and 16
-// are level). Launches with enough work (at 64 rows per task they would fill
-// 0.9 of the slots) take the hb minimising rounds * r * shares: long tasks on
-// every slot, or exactly two warps per scheduler, instead of a ragged count.
-// Smaller launches keep the round-1 latency model below, which measured
-// better there (B200, fp32 / fp64 Gcell/s, this model vs round 1: 2048^2
-// 352 / 252 vs 408 / 287; 4096^2 700 / 342 vs 653 / 287; 6144^2 985 vs 780;
-// 8192^2 1017 vs 944; config 4: the same hb either way).
-// (RD_HB=n fixes hb; RD_HB_MODEL=r01 | r02 forces one model.)
+// as 16) and a lone warp runs no faster than one of two. Pick the hb
+// minimising rounds * r * shares: long tasks on every slot, or exactly two
+// warps per scheduler, instead of a ragged count. Measured against the
+// round-1 latency model (kept below for lp_kernel), Gcell/s with the segment
+// graphs warm, fp32: 1536^2 536 vs 467, 2048^2 666 vs 575, 3072^2 874 vs 718,
+// 4096^2 958 vs 764, 6144^2 905 vs 779, 8192^2 993 vs 957; fp64: 3072^2 385
+// vs 310, 4096^2 392 vs 324; smaller grids and config 4: the same hb.
+// (RD_HB=n fixes hb; RD_HB_MODEL=r01 selects the round-1 model.)
 int pick_hb(const rd_sim* s, int n_strips, int64_t rows, int K, int64_t ctas, bool one_warp_ctas) {
   if (const char* e = getenv("RD_HB")) {
     int hb = atoi(e);
     if (hb >= 1) return hb;
   }
-  static const int force_model = [] {
+  static const bool old_model = [] {
     const char* e = getenv("RD_HB_MODEL");
-    return !e ? 0 : (std::string(e) == "r01" ? 1 : (std::string(e) == "r02" ? 2 : 0));
+    return e && std::string(e) == "r01";
   }();
-  const bool big = 10 * (int64_t)n_strips * s->B * ((rows + 63) / 64) >= 9 * ctas;
-  if (one_warp_ctas && force_model != 1 && (big || force_model == 2)) {
+  if (one_warp_ctas && !old_model) {
     int best = 1;
     double best_cost = 1e300;
     const int64_t hb_max = std::min<int64_t>(rows, 2048);
