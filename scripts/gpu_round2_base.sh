@@ -29,3 +29,6 @@ timeout 300 bash -c "$CMD4" > gpurun_out/plain_f64.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tb_kernel -s 12 -c 1 -o gpurun_out/prof_tb_f64 bash -c "$CMD4" > gpurun_out/ncu_f64.log 2>&1
 echo "f64 rc=$?"
 ncu -i gpurun_out/prof_tb_f64.ncu-rep --page raw --csv > gpurun_out/prof_tb_f64_raw.csv 2>/dev/null && rm -f gpurun_out/prof_tb_f64.ncu-rep
+# throughput against grid size with the default kernel choice (gz_kernel -> tb_kernel hand-over)
+timeout 600 python scripts/bench_sizes.py > gpurun_out/bench_sizes.log 2>&1; echo "sizes rc=$?"
+timeout 600 python scripts/bench_sizes.py --dtype f64 --sizes 128,256,512,1024,1536,2048,4096,8192 > gpurun_out/bench_sizes_f64.log 2>&1; echo "sizes f64 rc=$?"
