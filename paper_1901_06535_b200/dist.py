@@ -47,6 +47,8 @@ def unique_id(group=None) -> bytes:
     """rd_dist_unique_id on rank 0 of the torch.distributed group, broadcast
     to every rank (the only use of torch.distributed: the rendezvous)."""
     import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return rd_dist_unique_id()  # a world of one process: nothing to broadcast
     obj = [rd_dist_unique_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
     return obj[0]

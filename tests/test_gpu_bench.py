@@ -44,6 +44,10 @@ def test_bench_line_has_the_contract_keys():
     assert e["pipeline"] == 2 and e["steps"] == 3 and e["serial"]["value"] > 0 and e["serial"]["steps"] == 1
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    # config 4's phi is one value: a kernel parameter; the streamed rate goes beside the line's value
+    assert d["phi_uniform"] is True and d["roofline"]["kernel"].endswith(",uphi>")
+    assert d["phi_streamed"]["value"] > 0 and d["phi_streamed"]["phi_uniform"] == 0
+    assert d["fp64_large"]["gcell_updates_per_s"] > 0
     # configs[0..2] in both precisions, with the paper's outcomes
     pc = d["per_config"]
     assert len(pc) == 6 and {x["dtype"] for x in pc} == {"float32", "float64"}
@@ -74,6 +78,17 @@ def test_bench_n2_line_as_threads_on_one_gpu():
     assert d["halo_exchanges_rank0"] > 0
     s = d["strong"]
     assert s["value"] > 0 and s["config"]["grid"] == [8192, 8192] and s["roofline"]["achieved"] > 0
+
+
+def test_strong_line_at_one_gpu():
+    """--scaling strong at N = 1: the strong line's N = 1 point through a
+    world-of-one rd_create_dist handle (no process group: the rendezvous id is
+    made locally), on a reduced grid."""
+    d = _line(["--scaling", "strong", "--strong-grid", "4096", "--strong-timesteps", "8", "--steps", "3",
+               "--warmup", "3"])
+    assert d["n_gpus"] == 1 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["grid"] == [4096, 4096] and d["roofline"]["achieved"] > 0
+    assert d["roofline"]["kernel"] == "tb_kernel<float,K=4>"  # obstacles, a dist handle: the phi plane is streamed
 
 
 def test_reference_arm_line():
