@@ -12,8 +12,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r02"
 H = W = 16384
 rows = []
-for K in range(1, 9):
-    jf, cf = (os.path.join(ROOT, "gpurun_out", f"kt_{K}.{x}") for x in ("json", "csv"))
+# KT_TAG of scripts/gpu_ktable.sh: "s" = RD_TB_UPHI=0 (phi plane streamed), "u" = the default
+# (config 4's one-valued phi as a kernel parameter, K <= 4), "" = untagged.
+for tag, K in [(t, k) for t in ("s", "u", "") for k in range(1, 9)]:
+    jf, cf = (os.path.join(ROOT, "gpurun_out", f"kt{tag}_{K}.{x}") for x in ("json", "csv"))
     if not (os.path.exists(jf) and os.path.exists(cf)):
         continue
     line = json.loads(open(jf).read().strip().splitlines()[-1])
@@ -35,8 +37,11 @@ for K in range(1, 9):
     cells = H * W * K  # one launch = K steps over the whole grid
     dram = (avg("dram__bytes_read.sum") or 0) + (avg("dram__bytes_write.sum") or 0)
     inst = avg("smsp__inst_executed.sum")
-    model = (12 * (120 + 2 * K) / 120 + 8) / K  # SURVEY §8(d) B_eff(k) for 120 output columns per strip
-    rows.append({"K": K, "gcell_per_s": line["value"], "sm_mhz": line["clocks"]["sm_mhz"],
+    # SURVEY §8(d) B_eff(k) for 120 output columns per strip: u, v (and phi when streamed) read with the
+    # 2K-column halo, u', v' written once
+    model = ((8 if line.get("phi_uniform") else 12) * (120 + 2 * K) / 120 + 8) / K
+    rows.append({"K": K, "phi": {"s": "streamed", "u": "parameter when uniform (K <= 4)", "": "default"}[tag],
+                 "phi_uniform_path": line.get("phi_uniform"), "gcell_per_s": line["value"], "sm_mhz": line["clocks"]["sm_mhz"],
                  "ncu_launch_s": avg("gpu__time_duration.sum"),
                  "dram_bytes_per_launch": dram, "dram_bytes_per_cell_update": dram / cells,
                  "model_bytes_per_cell_update": model,
@@ -45,7 +50,9 @@ for K in range(1, 9):
                  "launches_averaged": len(m.get("dram__bytes_read.sum", []))})
 out = {"what": "tb_kernel<float,K> on config 4 (16384^2 fp32): rate from a plain bench run "
                "(--timesteps 60 --steps 3), DRAM bytes / instructions per cell-update from ncu over three "
-               "launches of the same command (--clock-control none); cell-updates per launch = 16384^2 x K",
+               "launches of the same command (--clock-control none); cell-updates per launch = 16384^2 x K. "
+               "Re-measured on the final round-2 kernel (row-triple rings, UPHI); the short runs stay under the "
+               "power cap, so sm_mhz is the maximum",
        "command": "bash scripts/gpu_ktable.sh", "rows": rows}
 dst = os.path.join(ROOT, "profiles", f"{rnd}_ktable.json")
 json.dump(out, open(dst, "w"), indent=1)
