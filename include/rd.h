@@ -155,7 +155,9 @@ typedef struct {
   int32_t batch, dtype, halo, tb_depth;
   int32_t rank, world;    /* dist handles: this rank of world; else 0 of 1 */
   int32_t transport;      /* RD_TRANSPORT_*: how a dist handle's halos travel */
-  int32_t pad;
+  int32_t flag_selftest;  /* multi-process dist handles, world > 1: the create-time test of the stream-ordered
+                             flag words across processes: 1 passed (P2P transport), -1 failed (NCCL send/recv
+                             instead); 0 = not run (world 1, in-process group, mapping failed earlier) */
 } rd_geometry;
 
 /* ---- lifecycle ---- */
@@ -210,6 +212,17 @@ int rd_get_geometry(const struct rd_sim* sim, rd_geometry* out);
  *                      NCCL unique id; make it on one rank and broadcast the
  *                      128 bytes, e.g. with torch.distributed). RD_ENCCL if
  *                      libnccl.so.2 cannot be loaded.
+ *   rd_dist_shm_id     a rendezvous id for ranks that are processes of THIS
+ *                      box, without NCCL: the rendezvous and the per-rd_step
+ *                      flag reduction go through a POSIX shared-memory
+ *                      segment the call creates (unlinked once every rank has
+ *                      joined); halos travel by the same copy-engine push.
+ *                      Ranks may share a device (that is how the
+ *                      cross-process protocol is tested on one GPU). There is
+ *                      no send/recv fallback: rd_create_dist fails (RD_ECUDA)
+ *                      if a peer mapping or its flag words do not work. A
+ *                      rank that waits longer than RD_DIST_TIMEOUT_S (300)
+ *                      for the others fails with RD_ENCCL, as do they.
  *   rd_dist_local_id   a rendezvous id for ranks that are host threads of
  *                      THIS process (no NCCL; ranks may share a device, e.g.
  *                      to test on one GPU; distinct devices need peer access).
@@ -226,8 +239,9 @@ int rd_get_geometry(const struct rd_sim* sim, rd_geometry* out);
  * a checkpoint; blocks of <= halo steps, each with its halo exchange (u and v
  * send rows straight into the neighbours' ghost rows by copy-engine
  * cudaMemcpyAsync over CUDA IPC / peer mappings, ordered by stream-ordered
- * counters, overlapped with the interior rows; RD_DIST_TRANSPORT=nccl or a
- * failed peer mapping selects grouped ncclSend/ncclRecv instead); one fault /
+ * counters, overlapped with the interior rows; RD_DIST_TRANSPORT=nccl, a
+ * failed peer mapping, or a failed create-time test of those counters between
+ * the processes selects grouped ncclSend/ncclRecv instead); one fault /
  * guard flag OR over the ranks (ncclAllReduce); on a fault every rank replays
  * step by step and stops at the first failing step, reporting the global first
  * cell. Results are bitwise those of one rd_create handle of the whole grid.
@@ -244,6 +258,7 @@ int rd_get_geometry(const struct rd_sim* sim, rd_geometry* out);
  * halo), RD_ENCCL, RD_ECUDA, RD_ENOMEM, RD_ENONFINITE (phi). */
 int rd_dist_unique_id(uint8_t id[128]);
 int rd_dist_local_id(uint8_t id[128]);
+int rd_dist_shm_id(uint8_t id[128]);
 int rd_create_dist(const rd_grid* global, const rd_params* params, const void* phi_rows, int32_t rank,
                    int32_t world, const uint8_t id[128], struct rd_sim** out);
 

@@ -23,7 +23,7 @@ __all__ = ["RDError", "Sim", "rd_params_default", "rd_create", "rd_create_slab",
            "rd_step", "rd_read_fields", "rd_write_fields", "rd_probe", "rd_probe_latch", "rd_probe_result",
            "rd_get_step", "rd_get_fault", "rd_checkpoint", "rd_step_unchecked", "rd_step_begin", "rd_step_finish", "RD_BLOCK_PUSH", "rd_plane_origins", "rd_set_peer", "rd_push_ghosts", "rd_flag_ptr", "rd_ipc_export", "rd_ipc_map", "rd_stream_signal", "rd_stream_wait", "rd_read_flags", "rd_restore", "rd_set_stream", "rd_row_ptr", "rd_timelapse", "rd_read_timelapse", "stream_handle", "rd_set_params", "rd_init_rest", "rd_fill_noise", "rd_paint_phi", "rd_get_stats", "rd_set_profiling",
            "rd_reset_stats", "rd_last_error", "load", "rd_get_geometry", "rd_arena_bytes", "rd_create_device",
-           "rd_field_ptr", "rd_dist_unique_id", "rd_dist_local_id", "rd_create_dist", "rd_write_fields_async",
+           "rd_field_ptr", "rd_dist_unique_id", "rd_dist_local_id", "rd_dist_shm_id", "rd_create_dist", "rd_write_fields_async",
            "rd_commit_fields", "rd_read_fields_async", "rd_io_wait"]
 
 _KIND = {"disc": RD_DISC, "rect": RD_RECT, "half_disc": RD_HALF_DISC}
@@ -145,7 +145,8 @@ def rd_destroy(h) -> None:
 
 def rd_get_geometry(h) -> dict:
     """Where the handle's rows sit: width, height (owned rows), height_global,
-    row0, pitch, batch, dtype, halo, tb_depth, rank, world, transport."""
+    row0, pitch, batch, dtype, halo, tb_depth, rank, world, transport,
+    flag_selftest."""
     g = _lib.rd_geometry()
     _check(load().rd_get_geometry(h, C.byref(g)), h)
     d = {k: getattr(g, k) for k, _ in g._fields_ if k != "pad"}
@@ -195,6 +196,14 @@ def rd_dist_local_id() -> bytes:
     return buf.raw
 
 
+def rd_dist_shm_id() -> bytes:
+    """128-byte rendezvous id for ranks that are processes of this box, without
+    NCCL (a POSIX shared-memory segment carries the control plane)."""
+    buf = C.create_string_buffer(128)
+    _check(load().rd_dist_shm_id(buf), create=True)
+    return buf.raw
+
+
 def rd_create_dist(width: int, height_global: int, phi_rows: np.ndarray | None, rank: int, world: int, uid: bytes, *,
                    batch: int = 1, dtype=np.float32, tb_depth: int = 0, flags: int = 0, params=None):
     """rd_create_dist (collective): rank's row slab of the global grid.
@@ -206,7 +215,7 @@ def rd_create_dist(width: int, height_global: int, phi_rows: np.ndarray | None, 
     rows = base + (1 if rank < extra else 0)
     _check_map(phi, dt, batch * rows * width, "phi_rows (owned rows)")
     if len(uid) != 128:
-        raise ValueError("uid must be the 128 bytes of rd_dist_unique_id / rd_dist_local_id")
+        raise ValueError("uid must be the 128 bytes of rd_dist_unique_id / rd_dist_local_id / rd_dist_shm_id")
     g = _lib.rd_grid(width, height_global, batch, _DT[dt], tb_depth, flags, 0)
     p = params or rd_params_default()
     h = C.c_void_p()

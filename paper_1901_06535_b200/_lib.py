@@ -58,7 +58,7 @@ class rd_geometry(C.Structure):
                 ("pitch", C.c_int64), ("phi_rows_lo", C.c_int64), ("phi_rows_hi", C.c_int64),
                 ("exchanges", C.c_int64), ("batch", C.c_int32), ("dtype", C.c_int32), ("halo", C.c_int32),
                 ("tb_depth", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("transport", C.c_int32),
-                ("pad", C.c_int32)]
+                ("flag_selftest", C.c_int32)]
 
 
 # (name, restype, argtypes) of every symbol include/rd.h declares
@@ -75,6 +75,7 @@ SYMBOLS = [
     ("rd_get_geometry", C.c_int, [P, C.POINTER(rd_geometry)]),
     ("rd_dist_unique_id", C.c_int, [P]),
     ("rd_dist_local_id", C.c_int, [P]),
+    ("rd_dist_shm_id", C.c_int, [P]),
     ("rd_create_dist", C.c_int, [C.POINTER(rd_grid), C.POINTER(rd_params), P, i32, i32, P, C.POINTER(P)]),
     ("rd_set_stream", C.c_int, [P, P]),
     ("rd_write_fields", C.c_int, [P, i32, P, P]),

@@ -41,7 +41,13 @@
 // on every rank), so they never need resetting.
 
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>  // types and enums only; the library is opened with dlopen
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <chrono>
 
 #include <condition_variable>
 #include <memory>
@@ -170,11 +176,90 @@ void local_allmax(LocalGroup& g, std::vector<uint64_t>& v) {
   v = g.result;
 }
 
+// ---- one-node process groups without NCCL (rd_dist_shm_id) -----------------
+// Ranks are processes of one box (one per GPU, or several sharing a GPU to
+// test the cross-process protocol on one device). The control plane -- the
+// record all-gather of the rendezvous and the per-rd_step flag reduction --
+// lives in a POSIX shared-memory segment; the data plane is the same copy-
+// engine push over CUDA IPC mappings as with NCCL (there is no send/recv
+// fallback here: a failed mapping is an error).
+constexpr char kShmMagic[8] = {'R', 'D', 'S', 'H', 'M', '0', '0', '1'};
+constexpr int kShmMaxWorld = 64, kShmWords = 64;
+
+struct ShmSeg {
+  std::atomic<uint32_t> world;    // set by the first rank to join
+  std::atomic<uint32_t> joined;   // ranks that have mapped the segment
+  std::atomic<uint32_t> left;     // ranks that have destroyed their handle
+  std::atomic<uint32_t> failed;   // a rank gave up (timeout): every waiter returns
+  std::atomic<uint64_t> arrived;  // monotone barrier counter: world per round
+  uint64_t slot[2][kShmMaxWorld][kShmWords];  // a rank's contribution, by round parity
+  unsigned char rec[kShmMaxWorld][256];       // the DistRec of every rank
+};
+
+struct ShmGroup {
+  ShmSeg* seg = nullptr;
+  std::string name;
+  int rank = 0, world = 1;
+  uint64_t round = 0;  // reductions this rank has completed
+};
+
+double shm_timeout_s() {
+  const char* e = getenv("RD_DIST_TIMEOUT_S");
+  const double t = e && *e ? atof(e) : 0.0;
+  return t > 0 ? t : 300.0;
+}
+
+std::string shm_name(const uint8_t id[128]) {
+  uint64_t tok;
+  std::memcpy(&tok, id + 8, 8);
+  char buf[64];
+  snprintf(buf, sizeof buf, "/rd_dist_%016llx", (unsigned long long)tok);
+  return buf;
+}
+
+// All ranks have arrived `round + 1` times. false on timeout or when another
+// rank failed (a dead peer must not hang the rest for good).
+bool shm_barrier(ShmGroup& g) {
+  ShmSeg& m = *g.seg;
+  const uint64_t target = (uint64_t)g.world * (g.round + 1);
+  m.arrived.fetch_add(1, std::memory_order_acq_rel);
+  const auto t0 = std::chrono::steady_clock::now();
+  const double limit = shm_timeout_s();
+  for (unsigned spins = 0; m.arrived.load(std::memory_order_acquire) < target; ++spins) {
+    if (m.failed.load(std::memory_order_acquire)) return false;
+    if (spins > 2000) usleep(50);
+    if ((spins & 1023) == 1023 &&
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+      m.failed.store(1, std::memory_order_release);
+      return false;
+    }
+  }
+  ++g.round;
+  return true;
+}
+
+// Element-wise MAX over the ranks. A rank writes its slot of parity
+// round % 2, all meet, each reduces all slots. A slot is rewritten two
+// rounds later, i.e. after a barrier every reader of this round has passed.
+bool shm_allmax(ShmGroup& g, std::vector<uint64_t>& v) {
+  ShmSeg& m = *g.seg;
+  const int par = (int)(g.round & 1);
+  for (size_t i = 0; i < v.size(); ++i) m.slot[par][g.rank][i] = v[i];
+  if (!shm_barrier(g)) return false;
+  for (size_t i = 0; i < v.size(); ++i) {
+    uint64_t x = 0;
+    for (int r = 0; r < g.world; ++r) x = std::max(x, m.slot[par][r][i]);
+    v[i] = x;
+  }
+  return true;
+}
+
 // word indices in each arena's 256-byte tail (words 0/1 belong to the
 // low-level RD_BLOCK_PUSH protocol, rd_flag_ptr): 4 + side = blocks the
 // neighbour on `side` allowed me to write into its ghost rows ("ready"),
 // 6 + side = blocks whose rows that neighbour delivered into mine ("landed")
-constexpr int kWordReady = 4, kWordLanded = 6;
+// 8 + side = the create-time self-test of the flag transport (dist_flag_selftest)
+constexpr int kWordReady = 4, kWordLanded = 6, kWordTest = 8;
 
 // What a rank publishes about its planes (NCCL rendezvous: all-gathered).
 struct DistRec {
@@ -192,6 +277,7 @@ struct DistState {
   int rank = 0, world = 1;
   bool local = false;
   std::shared_ptr<LocalGroup> lg;
+  ShmGroup* sg = nullptr;  // processes of one box without NCCL (rd_dist_shm_id)
   ncclComm_t comm = nullptr;
   bool p2p = true;  // copy-engine push into peer memory; false: NCCL send/recv
   bool flush = false;
@@ -214,6 +300,7 @@ struct DistState {
   uint64_t* d_red = nullptr;  // NCCL reduction scratch (64 x u64)
   int dev = 0;
   int64_t exchanges = 0;
+  int selftest = 0;  // dist_flag_selftest: 0 not run (world 1, in-process), 1 passed, -1 failed (NCCL transport)
 };
 
 uint32_t* my_words(rd_sim* s) {
@@ -246,6 +333,12 @@ int dist_allmax(rd_sim* s, std::vector<uint64_t>& v) {
     return RD_OK;
   }
   if (v.size() > 64) return set_err(s, RD_EINVAL, "reduction too large");
+  if (d->sg) {
+    if (!shm_allmax(*d->sg, v))
+      return set_err(s, RD_ENCCL, "shared-memory group: a rank failed or did not arrive within %.0f s (RD_DIST_TIMEOUT_S)",
+                     shm_timeout_s());
+    return RD_OK;
+  }
   RD_CUDA(s, cudaMemcpyAsync(d->d_red, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s->stream));
   RD_NCCL(s, nccl_api().AllReduce(d->d_red, d->d_red, v.size(), ncclUint64, ncclMax, d->comm, s->stream));
   RD_CUDA(s, cudaMemcpyAsync(v.data(), d->d_red, v.size() * 8, cudaMemcpyDeviceToHost, s->stream));
@@ -572,6 +665,45 @@ void set_neighbour(DistState* d, int side, const DistRec& r, int64_t delta) {
   p.words = nullptr;  // set by the caller: the neighbour's arena tail
 }
 
+// The block protocol of dist_block rests on two things that only ranks in
+// different processes exercise: a stream-ordered 32-bit write into the
+// neighbour's IPC-mapped arena, and a stream wait on a word that another
+// process (another device) writes. Try both once at create, on words of their
+// own, so that a platform without them falls back to NCCL send/recv here
+// instead of failing -- or hanging -- inside rd_step. A wait that is not
+// satisfied within RD_DIST_SELFTEST_MS (default 5000) is released by writing
+// the words from this rank itself.
+bool dist_flag_selftest(rd_sim* s) {
+  DistState* d = s->dist;
+  bool ok = true;
+  for (int side = 0; side < 2; ++side)
+    if (d->nb[side] >= 0 && ok)
+      ok = stream_write32(s, d->xs, d->peer[side].words + kWordTest + (1 - side), 1) == RD_OK;
+  for (int side = 0; side < 2; ++side)
+    if (d->nb[side] >= 0 && ok) ok = stream_wait32(s, d->xs, my_words(s) + kWordTest + side, 1, d->flush) == RD_OK;
+  const char* e = getenv("RD_DIST_SELFTEST_MS");
+  const double limit = (e && *e && atof(e) > 0 ? atof(e) : 5000.0) * 1e-3;
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaError_t q;
+  while ((q = cudaStreamQuery(d->xs)) == cudaErrorNotReady &&
+         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < limit)
+    usleep(200);
+  if (q == cudaErrorNotReady) {
+    ok = false;
+    static const uint32_t one = 1;
+    for (int side = 0; side < 2; ++side)
+      cudaMemcpyAsync(my_words(s) + kWordTest + side, &one, 4, cudaMemcpyHostToDevice, s->stream);
+    cudaStreamSynchronize(s->stream);
+    q = cudaStreamSynchronize(d->xs);
+  }
+  if (q != cudaSuccess) {
+    cudaGetLastError();
+    ok = false;
+  }
+  if (!ok) s->err.clear();
+  return ok;
+}
+
 int dist_rendezvous(rd_sim* s) {
   DistState* d = s->dist;
   // (each neighbour's word block sits at the end of ITS arena, whose size
@@ -603,26 +735,34 @@ int dist_rendezvous(rd_sim* s) {
     }
     return RD_OK;
   }
-  // NCCL: all-gather every rank's record, map the neighbours' arenas by IPC
-  const auto& N = nccl_api();
+  // all-gather every rank's record (NCCL, or the shared segment), map the
+  // neighbours' arenas by IPC
   DistRec mine = make_rec(s, true);
-  void* d_all = nullptr;
-  RD_CUDA(s, cudaMalloc(&d_all, (size_t)256 * (d->world + 1)));
   std::vector<unsigned char> all((size_t)256 * d->world);
-  std::vector<unsigned char> tmp(256, 0);
-  std::memcpy(tmp.data(), &mine, sizeof mine);
   int rc = RD_OK;
-  cudaError_t ce = cudaMemcpyAsync(static_cast<char*>(d_all) + 256 * d->world, tmp.data(), 256,
-                                   cudaMemcpyHostToDevice, s->stream);
-  ncclResult_t nr = ncclSuccess;
-  if (ce == cudaSuccess)
-    nr = N.AllGather(static_cast<char*>(d_all) + 256 * d->world, d_all, 256, ncclUint8, d->comm, s->stream);
-  if (ce == cudaSuccess && nr == ncclSuccess)
-    ce = cudaMemcpyAsync(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost, s->stream);
-  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s->stream);
-  cudaFree(d_all);
-  if (ce != cudaSuccess) return set_err(s, RD_ECUDA, "dist rendezvous: %s", cudaGetErrorString(ce));
-  if (nr != ncclSuccess) return set_err(s, RD_ENCCL, "dist rendezvous all-gather: %s", N.GetErrorString(nr));
+  if (d->sg) {
+    RD_CUDA(s, cudaStreamSynchronize(s->stream));  // the arena's zero fill, before anyone can write into it
+    std::memcpy(d->sg->seg->rec[d->rank], &mine, sizeof mine);
+    if ((rc = dist_barrier(s))) return rc;
+    std::memcpy(all.data(), d->sg->seg->rec, all.size());
+  } else {
+    const auto& N = nccl_api();
+    void* d_all = nullptr;
+    RD_CUDA(s, cudaMalloc(&d_all, (size_t)256 * (d->world + 1)));
+    std::vector<unsigned char> tmp(256, 0);
+    std::memcpy(tmp.data(), &mine, sizeof mine);
+    cudaError_t ce = cudaMemcpyAsync(static_cast<char*>(d_all) + 256 * d->world, tmp.data(), 256,
+                                     cudaMemcpyHostToDevice, s->stream);
+    ncclResult_t nr = ncclSuccess;
+    if (ce == cudaSuccess)
+      nr = N.AllGather(static_cast<char*>(d_all) + 256 * d->world, d_all, 256, ncclUint8, d->comm, s->stream);
+    if (ce == cudaSuccess && nr == ncclSuccess)
+      ce = cudaMemcpyAsync(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost, s->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s->stream);
+    cudaFree(d_all);
+    if (ce != cudaSuccess) return set_err(s, RD_ECUDA, "dist rendezvous: %s", cudaGetErrorString(ce));
+    if (nr != ncclSuccess) return set_err(s, RD_ENCCL, "dist rendezvous all-gather: %s", N.GetErrorString(nr));
+  }
   const char* tr = getenv("RD_DIST_TRANSPORT");
   if (tr && std::string(tr) == "nccl") p2p_ok = false;
   for (int side = 0; side < 2 && p2p_ok; ++side) {
@@ -639,13 +779,26 @@ int dist_rendezvous(rd_sim* s) {
     set_neighbour(d, side, r, (int64_t)(uintptr_t)mapped - (int64_t)r.base);
     d->peer[side].words = reinterpret_cast<uint32_t*>(static_cast<char*>(mapped) + r.arena_bytes - 256);
   }
-  // every rank must use the same transport
+  // every rank must use the same transport: first whether all mapped their
+  // neighbours, then whether the flag words work between them
   std::vector<uint64_t> v{p2p_ok ? 0ull : 1ull};
   if ((rc = dist_allmax(s, v))) return rc;
-  d->p2p = v[0] == 0;
+  p2p_ok = v[0] == 0;
+  if (p2p_ok && d->world > 1) {
+    v[0] = dist_flag_selftest(s) ? 0ull : 1ull;
+    if ((rc = dist_allmax(s, v))) return rc;
+    p2p_ok = v[0] == 0;
+    d->selftest = p2p_ok ? 1 : -1;
+  }
+  d->p2p = p2p_ok;
   if (!d->p2p) {
     for (void* m : d->ipc) cudaIpcCloseMemHandle(m);
     d->ipc.clear();
+    if (d->sg)
+      return set_err(s, RD_ECUDA,
+                     "shared-memory dist group: the peer mapping or its flag words are unavailable (CUDA IPC, "
+                     "cuStreamWriteValue32 / cuStreamWaitValue32 across processes) and this group has no NCCL "
+                     "fallback; use rd_dist_unique_id");
   }
   return RD_OK;
 }
@@ -659,6 +812,9 @@ int dist_create(const rd_grid* global, const rd_params* params, const void* phi_
   if (global->height < 3 || global->height < world)
     return set_err(nullptr, RD_EINVAL, "height must be >= 3 and >= world (SPEC.md:32)");
   const bool local = std::memcmp(id, kLocalMagic, 8) == 0;
+  const bool shm = std::memcmp(id, kShmMagic, 8) == 0;
+  if (shm && world > kShmMaxWorld)
+    return set_err(nullptr, RD_EINVAL, "a shared-memory group holds at most %d ranks", kShmMaxWorld);
   std::shared_ptr<LocalGroup> lg;
   if (local) {
     uint64_t tok;
@@ -676,7 +832,7 @@ int dist_create(const rd_grid* global, const rd_params* params, const void* phi_
     }
     if (lg->world != world) return set_err(nullptr, RD_EINVAL, "world %d differs from the group's %d", world, lg->world);
     if (lg->members[(size_t)rank]) return set_err(nullptr, RD_EINVAL, "rank %d already joined", rank);
-  } else if (!nccl_api().ok) {
+  } else if (!shm && !nccl_api().ok) {
     return set_err(nullptr, RD_ENCCL, "%s", nccl_api().why.c_str());
   }
   // rank's rows: the first H % G ranks get one extra row
@@ -695,6 +851,8 @@ int dist_create(const rd_grid* global, const rd_params* params, const void* phi_
   if (int rc = create_common(&g, params, nullptr, row0, H, depth, true, &s, nullptr, 0)) return rc;
   auto fail = [&](int rc) {
     std::string m = s->err;
+    // a shared-memory group must not wait for a rank that gave up
+    if (s->dist && s->dist->sg && s->dist->sg->seg) s->dist->sg->seg->failed.store(1);
     rd_destroy(s);
     return set_err(nullptr, rc, "%s", m.c_str());
   };
@@ -721,7 +879,27 @@ int dist_create(const rd_grid* global, const rd_params* params, const void* phi_
     s->err = "dist streams/events";
     return fail(RD_ECUDA);
   }
-  if (!local) {
+  if (shm) {
+    // map the segment rd_dist_shm_id made; the first rank in fixes the world
+    const std::string name = shm_name(id);
+    const int fd = shm_open(name.c_str(), O_RDWR, 0600);
+    void* m = fd >= 0 ? mmap(nullptr, sizeof(ShmSeg), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0) : MAP_FAILED;
+    if (fd >= 0) close(fd);
+    if (m == MAP_FAILED) {
+      s->err = "unknown shared-memory dist id (rd_dist_shm_id; ranks must run on the box that made it)";
+      return fail(RD_EINVAL);
+    }
+    d->sg = new ShmGroup();
+    d->sg->seg = static_cast<ShmSeg*>(m);
+    d->sg->name = name, d->sg->rank = rank, d->sg->world = world;
+    uint32_t w0 = 0;
+    if (!d->sg->seg->world.compare_exchange_strong(w0, (uint32_t)world) && w0 != (uint32_t)world) {
+      s->err = "world differs from the shared-memory group's";
+      return fail(RD_EINVAL);
+    }
+    // the name is no longer needed once every rank has mapped the segment
+    if (d->sg->seg->joined.fetch_add(1) + 1 == (uint32_t)world) shm_unlink(name.c_str());
+  } else if (!local) {
     ncclUniqueId uid;
     std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
     ncclResult_t r = nccl_api().CommInitRank(&d->comm, world, uid, rank);
@@ -767,6 +945,7 @@ void dist_geometry(const rd_sim* s, rd_geometry* out) {
   out->phi_rows_hi = s->H;
   out->transport = s->dist->local ? RD_TRANSPORT_LOCAL : (s->dist->p2p ? RD_TRANSPORT_P2P : RD_TRANSPORT_NCCL);
   out->exchanges = s->dist->exchanges;
+  out->flag_selftest = s->dist->selftest;
 }
 
 // Collective teardown: no rank frees its planes while a neighbour may still
@@ -778,9 +957,15 @@ void dist_destroy(rd_sim* s) {
   if (d->xs) cudaStreamSynchronize(d->xs);
   for (void* m : d->ipc) cudaIpcCloseMemHandle(m);
   d->ipc.clear();
-  const bool joined = d->local ? (d->lg && !d->lg->members.empty() && d->lg->members[d->rank] == s) : d->comm != nullptr;
-  if (joined && d->world > 1) dist_barrier(s);
+  const bool joined = d->local ? (d->lg && !d->lg->members.empty() && d->lg->members[d->rank] == s)
+                                : (d->sg ? d->sg->seg != nullptr : d->comm != nullptr);
+  if (joined && d->world > 1 && !(d->sg && d->sg->seg->failed.load())) dist_barrier(s);
   if (d->comm) nccl_api().CommDestroy(d->comm);
+  if (d->sg) {
+    if (d->sg->seg) munmap(d->sg->seg, sizeof(ShmSeg));
+    delete d->sg;
+    d->sg = nullptr;
+  }
   if (d->local && d->lg) {
     std::lock_guard<std::mutex> lk(d->lg->mu);
     if (!d->lg->members.empty() && d->lg->members[d->rank] == s && ++d->lg->left == d->lg->world) {
@@ -830,6 +1015,27 @@ int rd_dist_local_id(uint8_t id[128]) {
   std::lock_guard<std::mutex> lk(g_local_mu);
   g_local[tok] = std::make_shared<LocalGroup>();
   return RD_OK;
+}
+
+int rd_dist_shm_id(uint8_t id[128]) {
+  if (!id) return set_err(nullptr, RD_EINVAL, "id is NULL");
+  static std::atomic<uint64_t> counter{0};
+  std::random_device rdev;
+  std::memset(id, 0, 128);
+  std::memcpy(id, kShmMagic, 8);
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    const uint64_t tok = ((uint64_t)rdev() << 32 | rdev()) ^ (++counter * 0x9E3779B97F4A7C15ull) ^ (uint64_t)getpid();
+    std::memcpy(id + 8, &tok, 8);
+    const std::string name = shm_name(id);
+    const int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) continue;
+    // a fresh segment is zero-filled: every counter of ShmSeg starts at 0
+    const bool ok = ftruncate(fd, (off_t)sizeof(ShmSeg)) == 0;
+    close(fd);
+    if (ok) return RD_OK;
+    shm_unlink(name.c_str());
+  }
+  return set_err(nullptr, RD_ENOMEM, "could not create a POSIX shared-memory segment (/dev/shm)");
 }
 
 int rd_create_dist(const rd_grid* global, const rd_params* params, const void* phi_rows, int32_t rank,

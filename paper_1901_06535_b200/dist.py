@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import (rd_create_dist, rd_destroy, rd_dist_local_id, rd_dist_unique_id, rd_fill_noise, rd_get_geometry,
+from . import (rd_create_dist, rd_destroy, rd_dist_local_id, rd_dist_shm_id, rd_dist_unique_id, rd_fill_noise, rd_get_geometry,
                rd_get_stats, rd_init_rest, rd_paint_phi, rd_probe, rd_probe_latch, rd_probe_result, rd_read_fields,
                rd_set_stream, rd_step, rd_stimulate, rd_timelapse, rd_write_fields, stream_handle)
 
@@ -52,6 +52,13 @@ def unique_id(group=None) -> bytes:
     obj = [rd_dist_unique_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
     return obj[0]
+
+
+def shm_id() -> bytes:
+    """Rendezvous id for ranks that are processes of this box, without NCCL
+    (rd_dist_shm_id): make it in one process and hand the 128 bytes to the
+    others."""
+    return rd_dist_shm_id()
 
 
 def local_id() -> bytes:

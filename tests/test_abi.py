@@ -106,3 +106,25 @@ def test_dist_and_device_calls_validate_before_device():
     with pytest.raises(rd.RDError) as e:
         rd.rd_create_device(100, 50, 0, n, None)
     assert e.value.code == _lib.RD_EINVAL
+
+
+def test_shm_id_names_a_segment_of_this_box():
+    """rd_dist_shm_id creates the POSIX shared-memory segment its 128 bytes
+    name (the control plane of one-box process groups, no NCCL); a world
+    larger than a segment holds is refused before any device work."""
+    import os
+    import struct
+    uid = rd.rd_dist_shm_id()
+    assert uid[:8] == b"RDSHM001" and len(uid) == 128
+    name = lambda u: "/dev/shm/rd_dist_%016x" % struct.unpack("<Q", u[8:16])[0]  # noqa: E731
+    path = name(uid)
+    try:
+        assert os.path.exists(path) and os.path.getsize(path) > 64 * 256
+        other = rd.rd_dist_shm_id()
+        os.unlink(name(other))
+        assert other[8:16] != uid[8:16]
+        with pytest.raises(rd.RDError) as e:
+            rd.rd_create_dist(64, 1024, None, 0, 65, uid)
+        assert e.value.code == _lib.RD_EINVAL
+    finally:
+        os.unlink(path)
