@@ -183,7 +183,13 @@ class ProcCtx:
         return max_over_ranks(x, self.world)
 
     def uid(self) -> bytes:
-        from paper_1901_06535_b200.dist import unique_id
+        from paper_1901_06535_b200.dist import shm_id, unique_id
+        if os.environ.get("RD_BENCH_SHM") == "1" and self.world > 1:
+            # one-box process group without NCCL (rd_dist_shm_id): ranks may share a GPU
+            import torch.distributed as dist
+            obj = [shm_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            return obj[0]
         return unique_id()
 
 
@@ -662,7 +668,7 @@ def run_dist(args, ctx):
                                                 args.strong_grid),
                           "roofline": strong["roofline"], "transport": strong["geo"]["transport"]}
     if ctx.functional:
-        line["functional_check"] = ("RD_BENCH_THREADS: the ranks ran as threads on ONE GPU; the numbers are not "
+        line["functional_check"] = ("RD_BENCH_THREADS / RD_BENCH_SHM: the ranks shared a GPU; the numbers are not "
                                     "a measurement")
     return line
 
@@ -701,8 +707,15 @@ def run_ours(args):
     else:
         if world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        line = run_dist(args, ProcCtx(world, rank, local))
+            if os.environ.get("RD_BENCH_SHM") == "1":
+                # RD_BENCH_SHM=1: the torchrun launch on a box with fewer GPUs than ranks. torch's process
+                # group is gloo, librd's is the shared-memory one; the ranks' processes share devices.
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ctx = ProcCtx(world, rank, local)
+        ctx.functional = world > torch.cuda.device_count()
+        line = run_dist(args, ctx)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

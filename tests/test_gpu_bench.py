@@ -80,6 +80,41 @@ def test_bench_n2_line_as_threads_on_one_gpu():
     assert s["value"] > 0 and s["config"]["grid"] == [8192, 8192] and s["roofline"]["achieved"] > 0
 
 
+def test_bench_n2_under_torchrun_as_processes_on_one_gpu():
+    """The driver's N > 1 launch itself -- `python -m torch.distributed.run
+    --nproc-per-node 2 ... bench.py --gpus 2` -- with both rank processes on
+    this box's one GPU (RD_BENCH_SHM=1: torch's group is gloo and librd's the
+    shared-memory one, since NCCL needs a GPU per rank). The halos travel as
+    in the real launch: copy-engine pushes into the other process's IPC-mapped
+    arena, ordered by stream-ordered counters (transport p2p). Rank 0 alone
+    prints the line; a functional check, not a measurement."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, RD_BENCH_SHM="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--timesteps", "8",
+           "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--strong-grid", "8192", "--strong-timesteps", "8"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["steps"] == 3
+    assert d["transport"] == "p2p" and d["halo_exchanges_rank0"] > 0 and d["functional_check"]
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["strong"]["value"] > 0 and d["strong"]["transport"] == "p2p"
+    # the reference arm under the same launch: rank 0 alone works and prints
+    cmd2 = cmd[:cmd.index(os.path.join(ROOT, "bench.py")) + 1] + ["--impl", "reference", "--gpus", "2", "--steps", "1",
+                                                                 "--warmup", "0"]
+    cmd2[cmd2.index("--master-port") + 1] = str(port + 1 if port < 65000 else port - 1)
+    out = subprocess.run(cmd2, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["impl"] == "reference"
+
+
 def test_strong_line_at_one_gpu():
     """--scaling strong at N = 1: the strong line's N = 1 point through a
     world-of-one rd_create_dist handle (no process group: the rendezvous id is
