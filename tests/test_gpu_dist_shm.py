@@ -92,3 +92,64 @@ def test_process_ranks_equal_oracle(world, depth, dtype):
     assert_bitwise(U, ref.u, "u")
     assert_bitwise(V, ref.v, "v")
     assert {p[5] for p in parts} == {ref.first_fire[0]}
+
+
+def _fault_worker(rank, world, uid, steps, q):
+    try:
+        import torch
+        torch.cuda.set_device(0)
+        import paper_1901_06535_b200 as rd
+        from paper_1901_06535_b200.dist import DistSim
+        dtype = np.float32
+        s = DistSim(128, 96, rank, world, lambda b, r0, n: np.full((n, 128), 0.2, dtype), uid=uid, dtype=dtype)
+        s.write(0, lambda b, r0, n: noise_plane(n, 128, 0, seed=7, dtype=dtype, row0=r0),
+                lambda b, r0, n: noise_plane(n, 128, 1, seed=7, dtype=dtype, row0=r0))
+        s.stimulate(_FAULT_SHAPE, 1.0, 0)
+        code = 0
+        try:
+            s.step(steps)
+        except rd.RDError as e:
+            code = e.code
+        q.put((rank, s.row0, s.read_owned(0)[0], code, tuple(rd.rd_get_fault(s.h)), rd.rd_get_step(s.h)))
+        s.close()
+    except Exception as e:  # noqa: BLE001 - reported to the parent
+        q.put((rank, repr(e)))
+        raise
+
+
+_FAULT_SHAPE = {"kind": "half_disc", "cy2": 2 * 31, "cx2": 128, "r": 8, "dir": 1}  # straddles the rank 0/1 edge
+
+
+def test_process_ranks_fault_replay_stops_at_oracle_step():
+    """The collective PRECISE replay between processes: an unmasked stimulus
+    in a phi = 0.2 medium on noisy fields diverges; every rank process
+    restores, replays step by step (one exchange and one shared-memory
+    reduction per step) and stops at the oracle's step and global first cell
+    with the oracle's field."""
+    from paper_1901_06535_b200.dist import shm_id
+    import paper_1901_06535_b200 as rd
+    H, W, steps, world = 96, 128, 400, 3
+    dtype = np.float32
+    ref = oracle.run(noise_plane(H, W, 0, seed=7, dtype=dtype), noise_plane(H, W, 1, seed=7, dtype=dtype),
+                     np.full((H, W), 0.2, dtype), steps, events=[(_FAULT_SHAPE, 1.0, 0)])
+    assert ref.status == -4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    uid = shm_id()
+    procs = [ctx.Process(target=_fault_worker, args=(r, world, uid, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        parts = [q.get(timeout=240) for _ in range(world)]
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    for part in parts:
+        assert len(part) == 6, f"rank {part[0]} failed: {part[1]}"
+    parts.sort(key=lambda x: x[1])
+    for _, _, _, code, fault, step in parts:
+        assert code == rd.RD_ENONFINITE
+        assert (fault[0], fault[2], fault[3]) == ref.fault and step == ref.fault[0]
+    assert_bitwise(np.concatenate([p[2] for p in parts]), ref.u, "u at fault")
