@@ -4,6 +4,12 @@
  *   2. a two-rank in-process group (rd_dist_local_id, one pthread per rank,
  *      both ranks on device 0), fp32 and fp64: each rank owns half the rows,
  *      its halo rows travel to the other by cudaMemcpyAsync inside librd;
+ *   3. a two-rank group of PROCESSES (rd_dist_shm_id; the ranks are forked
+ *      before this process touches CUDA), fp32 and fp64: no NCCL, no Python;
+ *      each rank's arena is mapped into the other by CUDA IPC inside librd
+ *      and the halo rows are pushed into it (transport P2P, the create-time
+ *      flag self-test passing) -- the one-process-per-GPU protocol with both
+ *      processes on device 0;
  * each compared with the oracle's C library on the whole grid, bitwise.
  * Test program only: it links the oracle (tests/ may), the product does not.
  *   gcc -O2 -Iinclude -Ioracle tests/c/dist_c_demo.c -Lpaper_1901_06535_b200 -lrd -Loracle -lorc -lpthread */
@@ -12,6 +18,9 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <sys/mman.h>
+#include <sys/wait.h>
+#include <unistd.h>
 
 #include "rd.h"
 #include "rd_oracle.h"
@@ -40,6 +49,7 @@ typedef struct {
   unsigned char* u_global; /* rank writes its owned rows here */
   unsigned char* v_global;
   int rc;
+  int expect_p2p; /* ranks in different processes: copy-engine pushes over CUDA IPC, self-test passed */
 } job;
 
 static void* run_rank(void* arg) {
@@ -70,6 +80,10 @@ static void* run_rank(void* arg) {
   if (geo.row0 != row0 || geo.height != rows || geo.world != jb->world) {
     fprintf(stderr, "rank %d geometry\n", jb->rank);
     jb->rc = -100;
+  }
+  if (jb->expect_p2p && (geo.transport != RD_TRANSPORT_P2P || geo.flag_selftest != 1)) {
+    fprintf(stderr, "rank %d transport %d selftest %d\n", jb->rank, geo.transport, geo.flag_selftest);
+    jb->rc = -101;
   }
   rd_shape disc; /* centred on the slab edge of two ranks */
   memset(&disc, 0, sizeof disc);
@@ -121,7 +135,7 @@ static int run_group(int world, int dtype, const uint8_t* id, const char* what) 
   job jobs[4];
   pthread_t th[4];
   for (int r = 0; r < world; ++r) {
-    jobs[r] = (job){r, world, dtype, id, U, V, 0};
+    jobs[r] = (job){r, world, dtype, id, U, V, 0, 0};
     pthread_create(&th[r], NULL, run_rank, &jobs[r]);
   }
   int rc = 0;
@@ -138,8 +152,43 @@ static int run_group(int world, int dtype, const uint8_t* id, const char* what) 
   return bad;
 }
 
+/* The ranks as forked processes (before the parent initialises CUDA): the
+ * results come back through an anonymous shared mapping. */
+static int run_forked(int world, int dtype, const char* what) {
+  uint8_t id[128];
+  if (rd_dist_shm_id(id) != RD_OK) {
+    fprintf(stderr, "rd_dist_shm_id: %s\n", rd_create_error());
+    return 1;
+  }
+  const int esz = dtype == RD_F64 ? 8 : 4;
+  const size_t n = (size_t)H * W * esz;
+  unsigned char* sh = mmap(NULL, 2 * n, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_ANONYMOUS, -1, 0);
+  if (sh == MAP_FAILED) return 1;
+  pid_t pids[4];
+  for (int r = 0; r < world; ++r) {
+    pids[r] = fork();
+    if (pids[r] == 0) {
+      job jb = {r, world, dtype, id, sh, sh + n, 0, 1};
+      run_rank(&jb);
+      _exit(jb.rc ? 1 : 0);
+    }
+  }
+  int rc = 0;
+  for (int r = 0; r < world; ++r) {
+    int st = 0;
+    if (pids[r] < 0 || waitpid(pids[r], &st, 0) < 0 || !WIFEXITED(st) || WEXITSTATUS(st)) rc = 1;
+  }
+  if (rc) fprintf(stderr, "%s: rank error\n", what);
+  const int bad = rc || compare(dtype, sh, sh + n, what);
+  munmap(sh, 2 * n);
+  return bad;
+}
+
 int main(void) {
   uint8_t id[128];
+  /* first, while this process has no CUDA context to inherit */
+  if (run_forked(2, RD_F32, "2 rank processes, fp32")) return 1;
+  if (run_forked(2, RD_F64, "2 rank processes, fp64")) return 1;
   if (rd_dist_unique_id(id) != RD_OK) {
     fprintf(stderr, "rd_dist_unique_id: %s\n", rd_create_error());
     return 1;
@@ -159,6 +208,8 @@ int main(void) {
   memcpy(id + 8, "notatokn", 8);
   if (rd_create_dist(&g, &p, NULL, 0, 2, id, &s) != RD_EINVAL || s) return 1;
   if (rd_create_dist(&g, &p, NULL, 2, 2, id, &s) != RD_EINVAL || s) return 1;
-  printf("C dist ABI ok: world 1 over NCCL, 2 in-process ranks fp32 + fp64, bitwise equal to the oracle\n");
+  printf(
+      "C dist ABI ok: 2 rank processes (shared-memory group, IPC push) fp32 + fp64, world 1 over NCCL, 2 in-process "
+      "ranks fp32 + fp64, bitwise equal to the oracle\n");
   return 0;
 }

@@ -217,10 +217,11 @@ def test_c_abi_from_plain_c(tmp_path):
 
 
 def test_c_dist_abi_from_plain_c(tmp_path):
-    """The multi-GPU calls from C (tests/c/dist_c_demo.c): rd_dist_unique_id +
-    rd_create_dist at world 1 over NCCL, and two in-process ranks
-    (rd_dist_local_id, pthreads) on one device in fp32 and fp64 -- each
-    bitwise equal to the oracle's C library on the whole grid."""
+    """The multi-GPU calls from C (tests/c/dist_c_demo.c): two forked rank
+    processes over rd_dist_shm_id (CUDA IPC push, no NCCL, no Python),
+    rd_dist_unique_id + rd_create_dist at world 1 over NCCL, and two
+    in-process ranks (rd_dist_local_id, pthreads) on one device, in fp32 and
+    fp64 -- each bitwise equal to the oracle's C library on the whole grid."""
     root = os.path.dirname(HERE)
     exe = str(tmp_path / "dist_c_demo")
     lib, orc = os.path.join(root, "paper_1901_06535_b200"), os.path.join(root, "oracle")
