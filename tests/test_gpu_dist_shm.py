@@ -153,3 +153,24 @@ def test_process_ranks_fault_replay_stops_at_oracle_step():
         assert code == rd.RD_ENONFINITE
         assert (fault[0], fault[2], fault[3]) == ref.fault and step == ref.fault[0]
     assert_bitwise(np.concatenate([p[2] for p in parts]), ref.u, "u at fault")
+
+
+def test_missing_rank_fails_the_group_instead_of_hanging(monkeypatch):
+    """A rank whose peers never arrive gives up after RD_DIST_TIMEOUT_S with
+    RD_ENCCL (and marks the group failed, so late arrivals fail at once)."""
+    import time
+    import paper_1901_06535_b200 as rd
+    from paper_1901_06535_b200.dist import shm_id
+    monkeypatch.setenv("RD_DIST_TIMEOUT_S", "1.5")
+    uid = shm_id()
+    t = time.perf_counter()
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create_dist(64, 64, None, 0, 2, uid)
+    assert e.value.code == rd.RD_ENCCL and 1.0 < time.perf_counter() - t < 30
+    t = time.perf_counter()
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create_dist(64, 64, None, 1, 2, uid)  # the late rank: the segment is marked failed
+    assert e.value.code == rd.RD_ENCCL and time.perf_counter() - t < 10
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_create_dist(64, 64, None, 0, 2, uid)  # every rank has been and gone: the segment's name is unlinked
+    assert e.value.code == rd.RD_EINVAL
