@@ -520,7 +520,7 @@ int dist_run(rd_sim* s, int64_t n) {
   if (int rc = sync_probes(s)) return rc;
   const int64_t end = s->step + n;
   while (s->step < end) {
-    const int64_t k = std::min<int64_t>(s->halo, end - s->step);
+    const int64_t k = next_k(end - s->step, (int)s->halo);
     bool check = s->step + k >= end;  // the last block before the flag read
     for (const auto& ev : s->events) check = check || ev.at == s->step + k;  // ... or before a stamp
     if (int rc = dist_block(s, k, check)) return rc;
@@ -840,7 +840,8 @@ int dist_create(const rd_grid* global, const rd_params* params, const void* phi_
   const int64_t row0 = rank * base + std::min<int64_t>(rank, extra);
   const int64_t rows = base + (rank < extra ? 1 : 0);
   int depth = global->tb_depth;
-  if (depth == 0) depth = 4;
+  if (depth == 0)  // the single-GPU rule on this rank's slab (the ranks' row counts differ by at most one)
+    depth = auto_tb_for(global->dtype == RD_F64 ? 8 : 4, true, (int64_t)global->batch * (H / world) * global->width);
   if (world > 1 && rows < depth)
     return set_err(nullptr, RD_EINVAL, "slab of %lld rows is thinner than the halo (%d)", (long long)rows, depth);
   rd_grid g = *global;

@@ -27,8 +27,9 @@ cudaError_t launch_tb(const rdk::TBArgs<double>& a, int K, int mode, bool react,
                       unsigned grid, cudaStream_t st);
 // the uniform-phi tb_kernel is instantiated for K <= 4, reaction on, in the
 // default fast mode of the precision (fp32: guard-free 4-op division; fp64: FOLD)
+constexpr bool tb_uphi_depth(bool f32, int K) { return K <= 4 || (f32 && K <= 7); }
 inline bool tb_uphi_ok(bool f32, int K, int mode, bool react, bool lp) {
-  return K <= 4 && react && !lp && mode == (f32 ? rdk::MODE_FOLD_DIV4_NG : rdk::MODE_FOLD);
+  return tb_uphi_depth(f32, K) && react && !lp && mode == (f32 ? rdk::MODE_FOLD_DIV4_NG : rdk::MODE_FOLD);
 }
 
 // cr_kernel over `batch` clusters of cs CTAs with `smem` dynamic shared memory

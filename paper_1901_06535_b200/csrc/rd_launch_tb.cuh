@@ -46,7 +46,7 @@ template <typename T, int K, bool REACT, int MODE>
 cudaError_t go(const rdk::TBArgs<T>& a, bool lp, int var, bool uphi, unsigned grid, cudaStream_t st, int* occ) {
   constexpr int V = 16 / (int)sizeof(T);
   if (uphi) {
-    if constexpr (K <= 4 && REACT && has_variants<T, MODE>()) {
+    if constexpr (rdl::tb_uphi_depth(sizeof(T) == 4, K) && REACT && has_variants<T, MODE>()) {
       if (lp) return cudaErrorInvalidValue;
       switch (var) {
         case rdk::TB_LEAN: return go_uphi<T, K, REACT, MODE, rdk::TB_LEAN>(a, grid, st, occ);

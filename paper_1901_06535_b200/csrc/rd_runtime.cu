@@ -270,17 +270,39 @@ rdk::Consts<T> make_consts(const rd_params& p) {
   return k;
 }
 
-// Default temporal-blocking depth: 4, except for small fp64 batches (at most
-// 2^22 cells, single-GPU handles) where tb_kernel is launch/latency bound
-// and one more step per launch pays (configs 2/3 fp64 on tb_kernel, B200
-// sweep of depth x row block: depth 5 +13% on both).
-int auto_tb(const rd_sim* s) {
+// Default temporal-blocking depth. 4, except:
+// - small fp64 batches (at most 2^22 cells, single-GPU handles), where
+//   tb_kernel is launch/latency bound and one more step per launch pays
+//   (configs 2/3 fp64 on tb_kernel, B200 sweep of depth x row block: depth 5
+//   +13% on both);
+// - large fp32 grids (at least 2^26 cells on this handle): 6. In a run long
+//   enough to reach the 1 kW power cap the SM clock is set by energy per
+//   cell-update, and DRAM traffic is the part depth controls: sustained on
+//   16384^2, phi as a parameter, depth 4 / 5 / 6 / 7 = 1057 / 1113 / 1133 /
+//   1128 Gcell/s at 1778 / 1927 / 1965 / 1965 MHz; phi streamed 956 / 1044 /
+//   1049 / 1058; 8192^2 1065 -> 1095 and 961 -> 1022 (depth 7); 65536^2 (120
+//   GB) 859 -> 992. Below 2^26 cells depth 4 ties or wins (4096^2), and fp64
+//   is FP64-pipe bound at any depth (419 -> 407). DESIGN.md §5.2.
+constexpr int64_t kDeepCells = (int64_t)1 << 26;
+int auto_tb_for(int esz, bool slab, int64_t cells) {
   if (const char* e = getenv("RD_TB_DEPTH")) {
     int k = atoi(e);
     if (k >= 1 && k <= RD_MAX_TB) return k;
   }
-  if (s->esz == 8 && !s->slab && s->B * s->H * s->W <= (int64_t)1 << 22) return 5;
+  if (esz == 8 && !slab && cells <= (int64_t)1 << 22) return 5;
+  if (esz == 4 && cells >= kDeepCells) return 6;
   return 4;
+}
+int auto_tb(const rd_sim* s) { return auto_tb_for((int)s->esz, s->slab, s->B * s->H * s->W); }
+
+// Steps of the next launch of a segment with `remaining` steps at depth
+// kmax: the segment is cut into ceil(remaining / kmax) launches of nearly
+// equal depth (50 steps at depth 6: 6 6 6 6 6 5 5 5 5, not 8 x 6 + 2), since
+// shallow launches run at a fraction of the deep ones' rate. Results do not
+// depend on the cuts (bitwise).
+int next_k(int64_t remaining, int kmax) {
+  const int64_t n = (remaining + kmax - 1) / kmax;
+  return (int)((remaining + n - 1) / n);
 }
 
 template <typename T>
@@ -1082,7 +1104,7 @@ int run_blocks(rd_sim* s, int64_t next, int kmax) {
                      !s->graphs_broken && next - s->step >= 2 * kmax;
   if (!graph) {
     while (s->step < next) {
-      const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      const int k = next_k(next - s->step, kmax);
       s->lean_launch = s->step + k < next;  // the segment's last launch checks
       const int rc = launch_tb(s, k);
       s->lean_launch = false;
@@ -1098,7 +1120,7 @@ int run_blocks(rd_sim* s, int64_t next, int kmax) {
     // first occurrence of this segment shape: launch directly (a one-off
     // segment would not repay the capture)
     while (s->step < next) {
-      const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      const int k = next_k(next - s->step, kmax);
       s->lean_launch = s->step + k < next;  // the segment's last launch checks
       const int rc = launch_tb(s, k);
       s->lean_launch = false;
@@ -1119,7 +1141,7 @@ int run_blocks(rd_sim* s, int64_t next, int kmax) {
     int rc = RD_OK;
     if (cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) rc = RD_ECUDA;
     while (rc == RD_OK && s->step < next) {
-      const int k = (int)std::min<int64_t>(kmax, next - s->step);
+      const int k = next_k(next - s->step, kmax);
       s->lean_launch = s->step + k < next;  // the segment's last launch checks
       rc = launch_tb(s, k);
       s->lean_launch = false;

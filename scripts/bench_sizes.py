@@ -36,18 +36,22 @@ def run(n, dtype, steps, batch, obstacles=0):
     stream = torch.cuda.current_stream()
     sim.set_stream(stream)
     ms = None
-    for _ in range(4):  # the last run is reported (segment graph captured on the 2nd call, clocks up)
+    from bench import Clocks
+    for it in range(4):  # the last run is reported (segment graph captured on the 2nd call, clocks up)
         rd.rd_reset_stats(sim.h)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        e0.record(stream)
-        sim.step(steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        with Clocks(torch.cuda.current_device()) as clk:
+            e0.record(stream)
+            sim.step(steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
     st = sim.stats()
     sim.close()
-    return {"side": n, "width": w, "batch": batch, "dtype": np.dtype(dtype).name, "steps": steps, "device_ms": ms,
+    mhz = clk.summary()["sm_mhz"]
+    rate = batch * h * w * steps / (ms / 1e3) / 1e9
+    return {"sm_mhz": mhz, "gcell_per_s_per_ghz": rate / (mhz / 1e3) if mhz else None,"side": n, "width": w, "batch": batch, "dtype": np.dtype(dtype).name, "steps": steps, "device_ms": ms,
             "us_per_step": ms * 1e3 / steps, "gcell_updates_per_s": batch * h * w * steps / (ms / 1e3) / 1e9,
             "stencil_kernel": ["tb", "lp", "cr", "gz"][st["kernel"]], "tb_depth": st["tb_depth"],
             "phi_uniform": st["phi_uniform"], "obstacles": obstacles,

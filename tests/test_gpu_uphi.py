@@ -21,11 +21,12 @@ def _tb(monkeypatch):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
-@pytest.mark.parametrize("depth", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("depth", [1, 2, 3, 4, 6, 7, 8])
 @pytest.mark.parametrize("shape", [(67, 131), (40, 517), (131, 250)])
 def test_uniform_map_runs_the_parameter_variant_and_equals_the_oracle(shape, depth, dtype):
-    """Ragged shapes (one strip, several strips, W % V != 0) at every depth the
-    variant exists for (1-4) and one it does not (6: streams the plane)."""
+    """Ragged shapes (one strip, several strips, W % V != 0) at depths the
+    variant exists for (fp32: 1-7, fp64: 1-4) and some it does not (the plane
+    is streamed)."""
     H, W = shape
     phi = np.full((1, H, W), 0.054, dtype=dtype)
     u0 = noise_plane(H, W, 0, seed=7, dtype=dtype)
