@@ -252,3 +252,34 @@ def test_fast_division_f64_matches_ddiv_rn(divcheck64, q):
     r = json.loads(out.stdout)
     assert r["tested"] > 3_000_000_000
     assert r["mismatch_guarded"] == 0, r
+
+
+def test_default_depth_and_balanced_segment_cuts(monkeypatch):
+    """auto depth (DESIGN.md §5.2 "Depth"): fp32 handles of >= 2^26 cells take
+    depth 6, smaller ones and fp64 keep 4; a segment is cut into launches of
+    nearly equal depth (50 steps at depth 6: nine launches 6 6 6 6 6 5 5 5 5,
+    at depth 4: thirteen), and the cuts do not change the result."""
+    import numpy as np
+    import paper_1901_06535_b200 as rd
+    monkeypatch.setenv("RD_KERNEL", "tb")
+    monkeypatch.delenv("RD_TB_DEPTH", raising=False)
+
+    def stats(shape, dtype, steps, depth=0):
+        with rd.Sim(None, shape=shape, dtype=dtype, tb_depth=depth, flags=rd.RD_NO_GRAPH) as sim:
+            sim.paint_phi(0.054)
+            sim.fill_noise(seed=3)
+            rd.rd_reset_stats(sim.h)
+            sim.step(steps)
+            st = sim.stats()
+            return st, sim.read(0)
+
+    st, _ = stats((1, 8192, 8192), np.float32, 50)
+    assert st["tb_depth"] == 6 and st["step_launches"] == 9
+    st, _ = stats((1, 8192, 8191), np.float32, 8)
+    assert st["tb_depth"] == 4
+    st, _ = stats((1, 4096, 16384), np.float64, 8)
+    assert st["tb_depth"] == 4
+    st6, (u6, v6) = stats((1, 300, 500), np.float32, 50, depth=6)
+    st4, (u4, v4) = stats((1, 300, 500), np.float32, 50, depth=4)
+    assert st6["step_launches"] == 9 and st4["step_launches"] == 13
+    assert np.array_equal(u6, u4) and np.array_equal(v6, v4)
