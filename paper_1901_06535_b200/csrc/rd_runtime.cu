@@ -475,10 +475,8 @@ template <typename T>
 cudaError_t launch_stencil(rd_sim* s, int k, int in, int out, int32_t out_lo, int32_t out_hi, int mode, bool react) {
   constexpr int V = vec_of<T>();
   const bool lp = s->use_lp && k <= 4;
-  const int hx = ((k + V - 1) / V) * V, wo = 32 * V - 2 * hx;  // rdk::StripGeom<K, V>
   rdk::TBArgs<T> a;
   fill_args<T>(s, a, in, out, out_lo, out_hi, k);
-  a.n_strips = (int32_t)((s->W + wo - 1) / wo);
   // tb_kernel variant: timelapse samples, peer pushes and
   // PRECISE launches run the full kernel; otherwise the health check runs on
   // the launches that precede a stamp or the flag read (TB_CHECKED) and no
@@ -490,6 +488,13 @@ cudaError_t launch_stencil(rd_sim* s, int k, int in, int out, int32_t out_lo, in
   int var = rdk::TB_FULL;
   if (mode != rdk::MODE_PRECISE && !a.tl && !s->push_active && !force_full)
     var = s->lean_launch ? rdk::TB_LEAN : rdk::TB_CHECKED;
+  // rdk::StripGeom<K, V, VAR>: the lean/checked fp32 kernels of depth 5 and 6 run 6-column halos
+  // (the variants exist for the default fast mode only: any other mode runs the full kernel)
+  const bool half = !lp && V == 4 && (k == 5 || k == 6) && var != rdk::TB_FULL && react &&
+                    mode == rdk::MODE_FOLD_DIV4_NG;
+  const int hx = half ? 6 : ((k + V - 1) / V) * V, wo = 32 * V - 2 * hx;
+  // (half: strip i outputs columns [wo * i - 2, wo * i + wo - 2))
+  a.n_strips = (int32_t)((s->W + (half ? 2 : 0) + wo - 1) / wo);
   const bool uphi = s->phi_class_known && s->phi_uniform && rdl::tb_uphi_ok(sizeof(T) == 4, k, mode, react, lp);
   a.phi_u = (T)s->phi_u;
   const int64_t ctas = (int64_t)s->num_sms * rdl::occupancy_tb(sizeof(T) == 4, k, mode, react, lp, var, uphi);
