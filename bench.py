@@ -280,9 +280,12 @@ def load_traffic(workload: str, kernel: str, cells_per_launch: float):
         except Exception:
             continue
         for e in d.get("entries", []):
+            # the same launch size within 1%: a 1000-step segment at depth 6 is cut into 165 launches
+            # of 6 steps and 2 of 5 (5.99 on average); the capture is of a 6-step launch
             if (e.get("workload") == workload and e.get("kernel") == kernel
-                    and abs(e.get("cell_updates_per_launch", -1) - cells_per_launch) < 0.5):
-                return e["dram_bytes_per_launch"], os.path.relpath(f, ROOT)
+                    and abs(e.get("cell_updates_per_launch", -1) - cells_per_launch) <= 0.01 * cells_per_launch):
+                return e["dram_bytes_per_launch"], (f"{os.path.relpath(f, ROOT)} (a launch of "
+                                                    f"{e['cell_updates_per_launch']:.0f} cell-updates)")
     return None, None
 
 

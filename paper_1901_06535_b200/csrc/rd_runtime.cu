@@ -275,15 +275,19 @@ rdk::Consts<T> make_consts(const rd_params& p) {
 //   tb_kernel is launch/latency bound and one more step per launch pays
 //   (configs 2/3 fp64 on tb_kernel, B200 sweep of depth x row block: depth 5
 //   +13% on both);
-// - large fp32 grids (at least 2^26 cells on this handle): 6. In a run long
-//   enough to reach the 1 kW power cap the SM clock is set by energy per
-//   cell-update, and DRAM traffic is the part depth controls: sustained on
-//   16384^2, phi as a parameter, depth 4 / 5 / 6 / 7 = 1057 / 1113 / 1133 /
-//   1128 Gcell/s at 1778 / 1927 / 1965 / 1965 MHz; phi streamed 956 / 1044 /
-//   1049 / 1058; 8192^2 1065 -> 1095 and 961 -> 1022 (depth 7); 65536^2 (120
-//   GB) 859 -> 992. Below 2^26 cells depth 4 ties or wins (4096^2), and fp64
-//   is FP64-pipe bound at any depth (419 -> 407). DESIGN.md §5.2.
-constexpr int64_t kDeepCells = (int64_t)1 << 26;
+// - fp32 grids of at least 2^22 cells on this handle (2048^2; smaller ones
+//   run gz_kernel or are launch bound): 6. In a run long enough to reach the
+//   1 kW power cap the SM clock is set by energy per cell-update, and DRAM
+//   traffic is the part depth controls: sustained on 16384^2, phi as a
+//   parameter, depth 4 / 5 / 6 / 7 = 1057 / 1113 / 1133 / 1128 Gcell/s at
+//   1778 / 1927 / 1965 / 1965 MHz; phi streamed 956 / 1044 / 1049 / 1058;
+//   65536^2 (120 GB) 859 -> 992. With the 6-column halos of depths 5 and 6
+//   (StripGeom::HALF) depth 6 also wins on mid-size grids, parameter /
+//   streamed, depth 4 -> 6: 2048^2 666 -> 691 / 637 -> 654, 3072^2 869 -> 891
+//   / 831 -> 837, 4096^2 954 -> 982 / 912 -> 921, 6144^2 1018 -> 1091 / 915
+//   -> 1022, 8192^2 1039 -> 1105 / 957 -> 1006. fp64 is FP64-pipe bound at
+//   any depth (16384^2: 419 -> 407) and keeps 4. DESIGN.md §5.2.
+constexpr int64_t kDeepCells = (int64_t)1 << 22;
 int auto_tb_for(int esz, bool slab, int64_t cells) {
   if (const char* e = getenv("RD_TB_DEPTH")) {
     int k = atoi(e);

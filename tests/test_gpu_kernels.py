@@ -255,7 +255,7 @@ def test_fast_division_f64_matches_ddiv_rn(divcheck64, q):
 
 
 def test_default_depth_and_balanced_segment_cuts(monkeypatch):
-    """auto depth (DESIGN.md §5.2 "Depth"): fp32 handles of >= 2^26 cells take
+    """auto depth (DESIGN.md §5.2 "Depth"): fp32 handles of >= 2^22 cells take
     depth 6, smaller ones and fp64 keep 4; a segment is cut into launches of
     nearly equal depth (50 steps at depth 6: nine launches 6 6 6 6 6 5 5 5 5,
     at depth 4: thirteen), and the cuts do not change the result."""
@@ -273,9 +273,9 @@ def test_default_depth_and_balanced_segment_cuts(monkeypatch):
             st = sim.stats()
             return st, sim.read(0)
 
-    st, _ = stats((1, 8192, 8192), np.float32, 50)
+    st, _ = stats((1, 2048, 2048), np.float32, 50)
     assert st["tb_depth"] == 6 and st["step_launches"] == 9
-    st, _ = stats((1, 8192, 8191), np.float32, 8)
+    st, _ = stats((1, 2048, 2047), np.float32, 8)
     assert st["tb_depth"] == 4
     st, _ = stats((1, 4096, 16384), np.float64, 8)
     assert st["tb_depth"] == 4
