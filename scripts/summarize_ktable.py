@@ -39,8 +39,10 @@ for tag, K in [(t, k) for t in ("s", "u", "") for k in range(1, 9)]:
     inst = avg("smsp__inst_executed.sum")
     # SURVEY §8(d) B_eff(k) for 120 output columns per strip: u, v (and phi when streamed) read with the
     # 2K-column halo, u', v' written once
-    model = ((8 if line.get("phi_uniform") else 12) * (120 + 2 * K) / 120 + 8) / K
-    rows.append({"K": K, "phi": {"s": "streamed", "u": "parameter when uniform (K <= 4)", "": "default"}[tag],
+    # (K = 5, 6 run 116 output columns per 128-column strip, K = 4 120, K <= 3 120 with HX = 4)
+    wo = 116 if K in (5, 6) else 120
+    model = ((8 if line.get("phi_uniform") else 12) * 128 / wo + 8) / K
+    rows.append({"K": K, "phi": {"s": "streamed", "u": "parameter when uniform (fp32: K <= 7)", "": "default"}[tag],
                  "phi_uniform_path": line.get("phi_uniform"), "gcell_per_s": line["value"], "sm_mhz": line["clocks"]["sm_mhz"],
                  "ncu_launch_s": avg("gpu__time_duration.sum"),
                  "dram_bytes_per_launch": dram, "dram_bytes_per_cell_update": dram / cells,
@@ -51,8 +53,8 @@ for tag, K in [(t, k) for t in ("s", "u", "") for k in range(1, 9)]:
 out = {"what": "tb_kernel<float,K> on config 4 (16384^2 fp32): rate from a plain bench run "
                "(--timesteps 60 --steps 3), DRAM bytes / instructions per cell-update from ncu over three "
                "launches of the same command (--clock-control none); cell-updates per launch = 16384^2 x K. "
-               "Re-measured on the final round-2 kernel (row-triple rings, UPHI); the short runs stay under the "
-               "power cap, so sm_mhz is the maximum",
+               "Re-measured on the final round-2 kernel (row-triple rings, UPHI up to K = 7, 6-column halos at "
+               "K = 5 and 6); the short runs stay under the power cap, so sm_mhz is the maximum",
        "command": "bash scripts/gpu_ktable.sh", "rows": rows}
 dst = os.path.join(ROOT, "profiles", f"{rnd}_ktable.json")
 json.dump(out, open(dst, "w"), indent=1)
