@@ -263,6 +263,7 @@ def test_default_depth_and_balanced_segment_cuts(monkeypatch):
     import paper_1901_06535_b200 as rd
     monkeypatch.setenv("RD_KERNEL", "tb")
     monkeypatch.delenv("RD_TB_DEPTH", raising=False)
+    monkeypatch.setenv("RD_TB_DEEP", "1")  # librd reads it once per process: run this test in a fresh one
 
     def stats(shape, dtype, steps, depth=0):
         with rd.Sim(None, shape=shape, dtype=dtype, tb_depth=depth, flags=rd.RD_NO_GRAPH) as sim:
@@ -273,7 +274,7 @@ def test_default_depth_and_balanced_segment_cuts(monkeypatch):
             st = sim.stats()
             return st, sim.read(0)
 
-    st, _ = stats((1, 2048, 2048), np.float32, 50)
+    st, _ = stats((1, 2048, 2048), np.float32, 50, depth=6)
     assert st["tb_depth"] == 6 and st["step_launches"] == 9
     st, _ = stats((1, 2048, 2047), np.float32, 8)
     assert st["tb_depth"] == 4
