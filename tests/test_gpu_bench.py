@@ -123,7 +123,8 @@ def test_strong_line_at_one_gpu():
                "--warmup", "3"])
     assert d["n_gpus"] == 1 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["grid"] == [4096, 4096] and d["roofline"]["achieved"] > 0
-    assert d["roofline"]["kernel"] == "tb_kernel<float,K=4>"  # obstacles, a dist handle: the phi plane is streamed
+    assert d["roofline"]["kernel"] == "tb_kernel<float,K=6>"  # obstacles, a dist handle: the phi plane is streamed
+    # (fp32 handles of at least 2^22 cells default to depth 6)
 
 
 def test_reference_arm_line():

@@ -263,7 +263,7 @@ def test_default_depth_and_balanced_segment_cuts(monkeypatch):
     import paper_1901_06535_b200 as rd
     monkeypatch.setenv("RD_KERNEL", "tb")
     monkeypatch.delenv("RD_TB_DEPTH", raising=False)
-    monkeypatch.setenv("RD_TB_DEEP", "1")  # librd reads it once per process: run this test in a fresh one
+    monkeypatch.delenv("RD_TB_DEEP", raising=False)
 
     def stats(shape, dtype, steps, depth=0):
         with rd.Sim(None, shape=shape, dtype=dtype, tb_depth=depth, flags=rd.RD_NO_GRAPH) as sim:
